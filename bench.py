@@ -1,0 +1,299 @@
+#!/usr/bin/env python
+"""One VQE iteration (QSU + QR + EVC) of arXiv 2410.04252 on B200.
+
+Workload (BASELINE.json configs[1], "C2"): GateFabric, n=30 qubits, layers=4n=120
+(1,680 dense 4-qubit blocks, Rng seed 1), lazy flat_tiling schedule, then EVC
+of the synthetic Jordan-Wigner Hamiltonian gen_synthetic_jw(30, 1, max_span=10)
+with diagonalization.  At N GPUs the same 30-qubit state is sharded 2^g-way
+(p = N, strong scaling); the schedule's QRs move amplitudes over NVLink.
+
+A step = init_state + run_qsu + expectation through the public API
+(= evaluate_energy, dist_sim.cpp:357-363).  `value` is the step's device time
+(CUDA events on the libqrt stream, max over ranks); `e2e` is the host wall
+time of the same public-API step, which includes every host->device copy of
+the step's inputs (gate payloads, term masks) and the device->host read of the
+per-PE partial sums.  The 16-32 GiB state is far larger than L2, so no flush is
+needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+HBM_PEAK_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
+FP64_PEAK_NOMINAL = 37.0    # TFLOP/s, HGX B200 datasheet (296 TF / 8); not in MEASURED_PEAKS.json
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--qubits", type=int, default=30)
+    ap.add_argument("--layers", type=int, default=0, help="default 4n (PAPER.md:958)")
+    ap.add_argument("--span", type=int, default=10)
+    ap.add_argument("--schedule", choices=["flat", "hierarchical", "adhoc"], default="flat")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-qubits", type=int, default=24)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_PEAK_FALLBACK, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def workload(qb, args, p):
+    n = args.qubits
+    layers = args.layers or 4 * n
+    circuit = qb.gen_gatefabric(n, layers, 1, True)
+    deps = qb.build_dependency_graph(circuit)
+    shape = qb.ClusterShape.flat(p)
+    sched = {"flat": qb.flat_tiling, "hierarchical": qb.hierarchical_tiling, "adhoc": qb.adhoc_schedule}[args.schedule](
+        circuit, deps, shape)
+    terms = qb.gen_synthetic_jw(n, 1, args.span)
+    plan = qb.plan_evc(terms, n, shape, True, 8)
+    return n, layers, circuit, sched, terms, plan, shape
+
+
+def config_of(args, n, layers, n_gates, n_terms, p, qr_qsu=None, qr_evc=None):
+    return {"workload": f"C2 GateFabric {n}q layers={layers} ({n_gates} dense 4q gates, seed 1) + EVC of "
+                        f"gen_synthetic_jw({n},1,max_span={args.span}) ({n_terms} Pauli strings), {args.schedule} "
+                        f"schedule, p={p}",
+            "qubits": n, "pes": p, "schedule": args.schedule, "qr_qsu": qr_qsu, "qr_evc": qr_evc,
+            "l2": "inputs larger than L2 (state 16 B x 2^n)", "parallelism": f"state sharded {p}-way"}
+
+
+def cpu_baseline(args, n, p, n_gates, n_terms, layers):
+    """Reference CPU path (oracle/_ref, the unmodified reference) on a bounded
+    sample: n_s-qubit state, 6 gates + 24 strings, scaled linearly in 2^n."""
+    from oracle import ref as R
+
+    if not R.available():
+        return None
+    import multiprocessing
+
+    ns = min(args.cpu_sample_qubits, n)
+    workers = min(p, multiprocessing.cpu_count())
+    circ = R.Circuit.gatefabric(ns, 4, 1, True)
+    terms = R.Terms.jw(ns, 1, args.span)
+    t0 = time.time()
+    g, t = R.time_sample(circ, terms, p, workers, 6, 24)
+    wall = time.time() - t0
+    scale = float(1 << (n - ns))
+    per_iter = (g * n_gates + t * n_terms) * scale
+    return {"value": per_iter, "unit": "s", "cores": workers, "kind": "reference",
+            "sample": f"reference dist_sim (oracle/_ref) apply_gate_narrow x6 + expectation x24 strings at "
+                      f"n={ns}, p={p}, workers={workers} ({wall:.1f} s of CPU work); per-gate {g:.3g} s and "
+                      f"per-string {t:.3g} s scaled by 2^{n - ns} to {n_gates} gates + {n_terms} strings "
+                      f"(extrapolated, linear in 2^n)"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import ref as R
+    import paper_2410_04252_b200 as qb  # host-only use: generators + counts for the config echo
+
+    p = max(1, world)
+    n = args.qubits
+    layers = args.layers or 4 * n
+    n_gates = qb.gatefabric_block_count(n, layers)
+    n_terms = int(qb.synthetic_jw_term_count(n, args.span))
+    if not R.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libqrtile_ref.so not built"}))
+        return 0
+    vals = []
+    base = None
+    for i in range(args.warmup + args.steps):
+        base = cpu_baseline(args, n, p, n_gates, n_terms, layers)
+        if i >= args.warmup:
+            vals.append(base["value"])
+    v = statistics.median(vals)
+    base["value"] = v
+    line = {"metric": "VQE iteration time (QSU+EVC)", "value": v, "unit": "s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference", "config": config_of(args, n, layers, n_gates, n_terms, p),
+            "cpu_baseline": base, "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2410_04252_b200 as qb
+
+    rank, world, local = dist_env()
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    qb.init_distributed(device=local)
+    torch.cuda.set_device(local)
+    p = world
+    n, layers, circuit, sched, terms, plan, shape = workload(qb, args, p)
+    n_gates, n_terms = circuit.size(), len(terms)
+    hbm_peak, peak_kind = peaks()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def step(profile=False):
+        t0 = time.perf_counter()
+        st = qb.init_state(n, shape)
+        if profile:
+            st.profile(True)
+        stream = torch.cuda.ExternalStream(st.stream())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        qb.run_qsu(st, circuit, sched)
+        qr_qsu = len(st.qr_log)
+        energy = qb.expectation(st, plan, terms).real
+        e1.record(stream)
+        e1.synchronize()
+        wall = time.perf_counter() - t0
+        dev = e0.elapsed_time(e1) / 1e3
+        return st, energy, dev, wall, qr_qsu
+
+    for _ in range(args.warmup):
+        st, energy, _, _, _ = step()
+        del st
+    barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    devs, walls, launches = [], [], 0
+    for _ in range(args.steps):
+        st, energy, dev, wall, qr_qsu = step()
+        devs.append(dev)
+        walls.append(wall)
+        launches += sum(v["launches"] for v in st.stats().values())
+        qr_total = len(st.qr_log)
+        del st
+    barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    dev_t = max_over_ranks(statistics.mean(devs))
+    wall_t = max_over_ranks(statistics.mean(walls))
+
+    # one extra profiled (untimed) step: per-kernel-family event times for the roofline
+    st, _, _, _, _ = step(profile=True)
+    stats = st.stats()
+    del st
+    g = stats["gates"]
+    gate_ms = g["ms"] / max(1, g["launches"])
+    gate_bytes = g["bytes"] / max(1, g["launches"])
+    achieved = gate_bytes / (gate_ms / 1e3) / 1e9 if gate_ms > 0 else None
+    fp64 = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else None
+    qr = stats["qr"]
+    pa = stats["pauli"]
+    mat_bytes = sum(16 * (1 << (2 * op.arity())) for op in circuit.operators)
+    term_bytes = 8 * 5 * n_terms
+    d2h = 16 * p * max(1, len(plan.tiles))
+    if rank != 0:
+        return 0
+    line = {
+        "metric": "VQE iteration time (QSU+EVC)", "value": dev_t, "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_t * 1e3, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_of(args, n, layers, n_gates, n_terms, p, qr_qsu, qr_total - qr_qsu),
+        "energy": energy,
+        "e2e": {"value": wall_t, "unit": "s", "h2d_bytes_per_step": mat_bytes + term_bytes, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches // max(1, args.steps),
+        "clocks": clk,
+        "roofline": {"bound": "hbm", "kernel": "gate_pass_kernel (QSU)", "achieved": achieved, "peak": hbm_peak,
+                     "unit": "GB/s", "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
+                     "peak_kind": peak_kind, "avg_launch_ms": gate_ms, "algorithmic_bytes_per_launch": gate_bytes,
+                     "fp64_tflops": fp64, "fp64_peak_nominal": FP64_PEAK_NOMINAL,
+                     "fp64_frac": (fp64 / FP64_PEAK_NOMINAL) if fp64 else None},
+        "phases_ms": {"gates": g["ms"], "qr": qr["ms"], "pauli": pa["ms"], "misc": stats["misc"]["ms"],
+                      "gate_passes": g["launches"], "qr_launches": qr["launches"], "pauli_passes": pa["launches"],
+                      "qr_nvlink_gbs": (qr["bytes"] / (qr["ms"] / 1e3) / 1e9) if qr["ms"] > 0 else None},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, n, p, n_gates, n_terms, layers)
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

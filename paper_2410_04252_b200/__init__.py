@@ -1,0 +1,61 @@
+"""B200-native QSU / QR / EVC hot path of arXiv 2410.04252 (lazy qubit reordering).
+
+The package is a thin Python face over native code:
+
+* ``libqrt.so`` — hand-written sm_100a CUDA kernels behind the C ABI of
+  ``include/qrt.h`` (gate passes, NVLink reorder, batched Pauli expectation);
+* ``libqrtile_b200.so`` — the reference's C++ ``qrtile`` API re-implemented
+  host-side (schedulers bit-exact with the reference) on top of libqrt;
+* ``_qrtile`` — pybind11 bindings of that API.
+
+There is no CPU fallback: importing the package without the native libraries,
+or running on a machine without an sm_100 GPU, fails loudly at the first
+device call (``DeviceError``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+
+try:
+    from . import _qrtile  # noqa: F401  (loads libqrtile_b200.so and libqrt.so)
+except ImportError as exc:  # pragma: no cover - explicit, loud failure
+    raise ImportError(
+        "paper_2410_04252_b200 native extension is not built; run "
+        "`python -m paper_2410_04252_b200.build` (needs nvcc for sm_100a)") from exc
+
+from ._qrtile import *  # noqa: F401,F403,E402
+from ._qrtile import Error, DeviceError  # noqa: E402
+
+
+def libqrt_path() -> str:
+    return str(_PKG / "libqrt.so")
+
+
+def load_libqrt() -> ctypes.CDLL:
+    """The C ABI library itself (for direct ctypes callers and ABI tests)."""
+    return ctypes.CDLL(libqrt_path())
+
+
+def init_distributed(device: int | None = None):
+    """One process per GPU: read RANK/WORLD_SIZE/LOCAL_RANK, share the NCCL id
+    over torch.distributed (gloo, plumbing only) and create the libqrt
+    communicator.  Returns (rank, world, device)."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    dev = local if device is None else device
+    if world == 1:
+        _qrtile.init_device(0, 1, dev)
+        return 0, 1, dev
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        dist.init_process_group("gloo")
+    box = [_qrtile.device_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    _qrtile.init_device(rank, world, dev, box[0])
+    return rank, world, dev

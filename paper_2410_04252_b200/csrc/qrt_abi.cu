@@ -1,0 +1,458 @@
+// libqrt — C ABI entry points (include/qrt.h), device state management,
+// the one-process-per-GPU communicator (NCCL for barriers / gathers, CUDA IPC
+// for direct NVLink peer stores) and measurement plumbing.
+//
+// Reference mapping: qrt_state_create/set_zero <- init_state
+// (dist_sim.cpp:122-131); upload/download <- init_state(ref)/flatten
+// (:133-161, position order); qrt_norm <- DistributedState::norm (:115-120).
+
+#include <cstring>
+#include <mutex>
+
+#include "qrt_internal.h"
+
+namespace qrt {
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+qrt_status guarded(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return QRT_OK;
+    } catch (const Failure& e) {
+        g_last_error = e.what();
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host out of memory";
+        return QRT_ERR_OOM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return QRT_ERR_INVALID;
+    }
+}
+
+void require(bool ok, qrt_status s, const std::string& msg) {
+    if (!ok) fail(s, msg);
+}
+
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int dev) {
+        QRT_CUDA(cudaGetDevice(&prev));
+        if (prev != dev) QRT_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+__global__ void zero_state_kernel(amp_t* __restrict__ v, std::uint64_t count, int set_first) {
+    std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+    for (; i < count; i += stride) v[i] = make_double2((set_first && i == 0) ? 1.0 : 0.0, 0.0);
+}
+
+int grid_for(std::uint64_t items, int threads) {
+    int sms = 148;
+    std::uint64_t want = (items + threads - 1) / threads;
+    std::uint64_t cap = static_cast<std::uint64_t>(sms) * 8;
+    return static_cast<int>(want < cap ? (want == 0 ? 1 : want) : cap);
+}
+
+}  // namespace
+
+void fail(qrt_status s, const std::string& msg) { throw Failure(s, msg); }
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e == cudaSuccess) return;
+    qrt_status s = (e == cudaErrorMemoryAllocation) ? QRT_ERR_OOM
+                   : (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) ? QRT_ERR_NO_DEVICE
+                                                                                   : QRT_ERR_CUDA;
+    fail(s, std::string(cudaGetErrorString(e)) + " in " + what + " at " + file + ":" + std::to_string(line));
+}
+
+void nccl_check(ncclResult_t r, const char* what, const char* file, int line) {
+    if (r == ncclSuccess) return;
+    fail(QRT_ERR_NCCL, std::string(ncclGetErrorString(r)) + " in " + what + " at " + file + ":" + std::to_string(line));
+}
+
+ProfileScope::ProfileScope(qrt_state* s, int f) : st(s), fam(f) {
+    if (st->profile) QRT_CUDA(cudaEventRecord(st->ev0, st->stream));
+}
+ProfileScope::~ProfileScope() noexcept(false) {
+    if (!st->profile) return;
+    QRT_CUDA(cudaEventRecord(st->ev1, st->stream));
+    QRT_CUDA(cudaEventSynchronize(st->ev1));
+    float ms = 0.f;
+    QRT_CUDA(cudaEventElapsedTime(&ms, st->ev0, st->ev1));
+    st->stats[fam].ms += ms;
+}
+
+void ensure_alt(qrt_state* st) {
+    if (!st->bufs[1].empty() && st->bufs[1][0] != nullptr) return;
+    st->bufs[1].assign(static_cast<std::size_t>(st->pe_count), nullptr);
+    for (int i = 0; i < st->pe_count; ++i) QRT_CUDA(cudaMalloc(&st->bufs[1][static_cast<std::size_t>(i)], st->amps * sizeof(amp_t)));
+    // single-process: the peer tables are the local buffers
+    for (int b = 0; b < 2; ++b)
+        for (int i = 0; i < st->pe_count; ++i)
+            st->peer[b][static_cast<std::size_t>(st->pe_begin + i)] = st->bufs[b][static_cast<std::size_t>(i)];
+}
+
+void* ensure_ops(qrt_state* st, std::size_t bytes) {
+    if (bytes > st->ops_cap) {
+        if (st->d_ops) QRT_CUDA(cudaFree(st->d_ops));
+        std::size_t cap = bytes < (1u << 20) ? (1u << 20) : bytes + bytes / 2;
+        QRT_CUDA(cudaMalloc(&st->d_ops, cap));
+        st->ops_cap = cap;
+    }
+    return st->d_ops;
+}
+
+void* ensure_pinned(qrt_state* st, std::size_t bytes) {
+    if (bytes > st->pinned_cap) {
+        if (st->h_pinned) {
+            QRT_CUDA(cudaStreamSynchronize(st->stream));
+            QRT_CUDA(cudaFreeHost(st->h_pinned));
+        }
+        std::size_t cap = bytes < (1u << 20) ? (1u << 20) : bytes + bytes / 2;
+        QRT_CUDA(cudaMallocHost(&st->h_pinned, cap));
+        st->pinned_cap = cap;
+    }
+    return st->h_pinned;
+}
+
+double* ensure_red(qrt_state* st, std::size_t doubles) {
+    if (doubles > st->red_cap) {
+        if (st->d_red) QRT_CUDA(cudaFree(st->d_red));
+        QRT_CUDA(cudaMalloc(&st->d_red, doubles * sizeof(double)));
+        st->red_cap = doubles;
+    }
+    return st->d_red;
+}
+
+void barrier_on_stream(qrt_state* st) {
+    if (!st->comm || st->comm->world == 1) return;
+    QRT_NCCL(ncclAllReduce(st->d_flag, st->d_flag, 1, ncclInt32, ncclSum, st->comm->nccl, st->stream));
+}
+
+}  // namespace qrt
+
+using namespace qrt;
+
+// ============================================================================
+extern "C" {
+
+const char* qrt_last_error(void) { return g_last_error.c_str(); }
+int qrt_abi_version(void) { return QRT_ABI_VERSION; }
+
+qrt_status qrt_device_count(int* out) {
+    return guarded([&] {
+        require(out != nullptr, QRT_ERR_INVALID, "null out");
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            *out = 0;
+            return;
+        }
+        int good = 0;
+        for (int d = 0; d < n; ++d) {
+            cudaDeviceProp prop{};
+            if (cudaGetDeviceProperties(&prop, d) == cudaSuccess && prop.major == 10) ++good;
+        }
+        *out = good;
+    });
+}
+
+qrt_status qrt_comm_unique_id(unsigned char id[128]) {
+    return guarded([&] {
+        static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+        ncclUniqueId uid;
+        QRT_NCCL(ncclGetUniqueId(&uid));
+        std::memcpy(id, &uid, 128);
+    });
+}
+
+qrt_status qrt_comm_init(int rank, int world, int device, const unsigned char id[128], qrt_comm** out) {
+    return guarded([&] {
+        require(out && world >= 1 && rank >= 0 && rank < world, QRT_ERR_INVALID, "bad communicator arguments");
+        auto* c = new qrt_comm;
+        c->rank = rank;
+        c->world = world;
+        c->device = device;
+        DeviceGuard g(device);
+        if (world > 1) {
+            ncclUniqueId uid;
+            std::memcpy(&uid, id, 128);
+            QRT_NCCL(ncclCommInitRank(&c->nccl, world, uid, rank));
+        }
+        *out = c;
+    });
+}
+
+qrt_status qrt_comm_barrier(qrt_comm* comm) {
+    return guarded([&] {
+        require(comm != nullptr, QRT_ERR_INVALID, "null comm");
+        if (comm->world == 1) return;
+        DeviceGuard g(comm->device);
+        int* d = nullptr;
+        QRT_CUDA(cudaMalloc(&d, sizeof(int)));
+        QRT_NCCL(ncclAllReduce(d, d, 1, ncclInt32, ncclSum, comm->nccl, nullptr));
+        QRT_CUDA(cudaStreamSynchronize(nullptr));
+        QRT_CUDA(cudaFree(d));
+    });
+}
+
+qrt_status qrt_comm_destroy(qrt_comm* comm) {
+    return guarded([&] {
+        if (!comm) return;
+        if (comm->nccl) ncclCommDestroy(comm->nccl);
+        delete comm;
+    });
+}
+
+qrt_status qrt_state_create(int n, int p, int device, qrt_comm* comm, qrt_state** out) {
+    return guarded([&] {
+        require(out != nullptr, QRT_ERR_INVALID, "null out");
+        require(p >= 1 && (p & (p - 1)) == 0, QRT_ERR_CONFIG, "p must be a power of two");
+        require(n >= 1 && n <= 62, QRT_ERR_CONFIG, "qubit count out of range");
+        int g = __builtin_ctz(static_cast<unsigned>(p));
+        require(n - g >= 1, QRT_ERR_TOO_MANY_PES, "p = " + std::to_string(p) + " leaves no local qubit");
+        int world = comm ? comm->world : 1;
+        int rank = comm ? comm->rank : 0;
+        require(p % world == 0, QRT_ERR_CONFIG, "p must be a multiple of the world size");
+        int ndev = 0;
+        cudaError_t e = cudaGetDeviceCount(&ndev);
+        if (e != cudaSuccess || ndev == 0) {
+            cudaGetLastError();
+            fail(QRT_ERR_NO_DEVICE, "no CUDA device visible");
+        }
+        require(device >= 0 && device < ndev, QRT_ERR_NO_DEVICE, "device index out of range");
+        DeviceGuard dg(device);
+
+        auto st = new qrt_state;
+        st->n = n;
+        st->p = p;
+        st->nl = n - g;
+        st->device = device;
+        st->comm = comm;
+        st->pe_count = p / world;
+        require(st->pe_count <= kMaxLocalPEs, QRT_ERR_CONFIG, "too many PEs per process");
+        st->pe_begin = rank * st->pe_count;
+        st->amps = 1ull << st->nl;
+        try {
+            QRT_CUDA(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
+            QRT_CUDA(cudaEventCreate(&st->ev0));
+            QRT_CUDA(cudaEventCreate(&st->ev1));
+            QRT_CUDA(cudaMalloc(&st->d_flag, sizeof(int)));
+            QRT_CUDA(cudaMemsetAsync(st->d_flag, 0, sizeof(int), st->stream));
+            for (int b = 0; b < 2; ++b) {
+                st->bufs[b].assign(static_cast<std::size_t>(st->pe_count), nullptr);
+                st->peer[b].assign(static_cast<std::size_t>(p), nullptr);
+            }
+            const bool multi = comm && world > 1;
+            const int nb = multi ? 2 : 1;
+            for (int b = 0; b < nb; ++b)
+                for (int i = 0; i < st->pe_count; ++i)
+                    QRT_CUDA(cudaMalloc(&st->bufs[b][static_cast<std::size_t>(i)], st->amps * sizeof(amp_t)));
+            for (int b = 0; b < nb; ++b)
+                for (int i = 0; i < st->pe_count; ++i)
+                    st->peer[b][static_cast<std::size_t>(st->pe_begin + i)] = st->bufs[b][static_cast<std::size_t>(i)];
+            if (multi) {
+                // Exchange IPC handles of both buffers of every PE (all-gather).
+                const std::size_t per = static_cast<std::size_t>(2 * st->pe_count) * sizeof(cudaIpcMemHandle_t);
+                std::vector<cudaIpcMemHandle_t> mine(static_cast<std::size_t>(2 * st->pe_count));
+                for (int b = 0; b < 2; ++b)
+                    for (int i = 0; i < st->pe_count; ++i)
+                        QRT_CUDA(cudaIpcGetMemHandle(&mine[static_cast<std::size_t>(b * st->pe_count + i)],
+                                                     st->bufs[b][static_cast<std::size_t>(i)]));
+                char* d_all = nullptr;
+                QRT_CUDA(cudaMalloc(&d_all, per * static_cast<std::size_t>(world)));
+                QRT_CUDA(cudaMemcpyAsync(d_all + per * static_cast<std::size_t>(rank), mine.data(), per,
+                                         cudaMemcpyHostToDevice, st->stream));
+                QRT_NCCL(ncclAllGather(d_all + per * static_cast<std::size_t>(rank), d_all, per, ncclChar,
+                                       comm->nccl, st->stream));
+                std::vector<cudaIpcMemHandle_t> all(static_cast<std::size_t>(2 * st->pe_count * world));
+                QRT_CUDA(cudaMemcpyAsync(all.data(), d_all, per * static_cast<std::size_t>(world), cudaMemcpyDeviceToHost,
+                                         st->stream));
+                QRT_CUDA(cudaStreamSynchronize(st->stream));
+                QRT_CUDA(cudaFree(d_all));
+                for (int r = 0; r < world; ++r) {
+                    if (r == rank) continue;
+                    for (int b = 0; b < 2; ++b)
+                        for (int i = 0; i < st->pe_count; ++i) {
+                            void* ptr = nullptr;
+                            QRT_CUDA(cudaIpcOpenMemHandle(
+                                &ptr, all[static_cast<std::size_t>((r * 2 + b) * st->pe_count + i)],
+                                cudaIpcMemLazyEnablePeerAccess));
+                            st->peer[b][static_cast<std::size_t>(r * st->pe_count + i)] = static_cast<amp_t*>(ptr);
+                            st->ipc_opened.push_back(ptr);
+                        }
+                }
+            }
+            for (int i = 0; i < st->pe_count; ++i)
+                zero_state_kernel<<<grid_for(st->amps, 256), 256, 0, st->stream>>>(
+                    st->bufs[0][static_cast<std::size_t>(i)], st->amps, st->pe_begin + i == 0);
+            QRT_CUDA(cudaGetLastError());
+            st->stats[QRT_K_MISC].launches += static_cast<std::uint64_t>(st->pe_count);
+            QRT_CUDA(cudaStreamSynchronize(st->stream));
+            if (multi) {
+                barrier_on_stream(st);
+                QRT_CUDA(cudaStreamSynchronize(st->stream));
+            }
+        } catch (...) {
+            qrt_state_destroy(st);
+            throw;
+        }
+        *out = st;
+    });
+}
+
+qrt_status qrt_state_destroy(qrt_state* st) {
+    return guarded([&] {
+        if (!st) return;
+        DeviceGuard g(st->device);
+        if (st->stream) cudaStreamSynchronize(st->stream);
+        for (void* ptr : st->ipc_opened) cudaIpcCloseMemHandle(ptr);
+        for (int b = 0; b < 2; ++b)
+            for (auto* ptr : st->bufs[b])
+                if (ptr) cudaFree(ptr);
+        if (st->d_red) cudaFree(st->d_red);
+        if (st->d_ops) cudaFree(st->d_ops);
+        if (st->h_pinned) cudaFreeHost(st->h_pinned);
+        if (st->d_flag) cudaFree(st->d_flag);
+        if (st->ev0) cudaEventDestroy(st->ev0);
+        if (st->ev1) cudaEventDestroy(st->ev1);
+        if (st->stream) cudaStreamDestroy(st->stream);
+        delete st;
+    });
+}
+
+qrt_status qrt_state_info(const qrt_state* st, int* n, int* p, int* pe_begin, int* pe_count) {
+    return guarded([&] {
+        require(st != nullptr, QRT_ERR_INVALID, "null state");
+        if (n) *n = st->n;
+        if (p) *p = st->p;
+        if (pe_begin) *pe_begin = st->pe_begin;
+        if (pe_count) *pe_count = st->pe_count;
+    });
+}
+
+qrt_status qrt_state_set_zero(qrt_state* st) {
+    return guarded([&] {
+        require(st != nullptr, QRT_ERR_INVALID, "null state");
+        DeviceGuard g(st->device);
+        for (int i = 0; i < st->pe_count; ++i)
+            zero_state_kernel<<<grid_for(st->amps, 256), 256, 0, st->stream>>>(st->live(i), st->amps,
+                                                                               st->pe_begin + i == 0);
+        QRT_CUDA(cudaGetLastError());
+        st->stats[QRT_K_MISC].launches += static_cast<std::uint64_t>(st->pe_count);
+        QRT_CUDA(cudaStreamSynchronize(st->stream));
+    });
+}
+
+qrt_status qrt_state_upload(qrt_state* st, int pe, const double* amps) {
+    return guarded([&] {
+        require(st && amps, QRT_ERR_INVALID, "null argument");
+        require(pe >= st->pe_begin && pe < st->pe_begin + st->pe_count, QRT_ERR_INVALID, "PE not owned by this process");
+        DeviceGuard g(st->device);
+        QRT_CUDA(cudaMemcpyAsync(st->live(pe - st->pe_begin), amps, st->amps * sizeof(amp_t), cudaMemcpyHostToDevice,
+                                 st->stream));
+        QRT_CUDA(cudaStreamSynchronize(st->stream));
+    });
+}
+
+qrt_status qrt_state_download(const qrt_state* st, int pe, double* amps) {
+    return guarded([&] {
+        require(st && amps, QRT_ERR_INVALID, "null argument");
+        require(pe >= st->pe_begin && pe < st->pe_begin + st->pe_count, QRT_ERR_INVALID, "PE not owned by this process");
+        DeviceGuard g(st->device);
+        QRT_CUDA(cudaMemcpyAsync(amps, st->live(pe - st->pe_begin), st->amps * sizeof(amp_t), cudaMemcpyDeviceToHost,
+                                 st->stream));
+        QRT_CUDA(cudaStreamSynchronize(st->stream));
+    });
+}
+
+qrt_status qrt_apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, const double* mats,
+                           const unsigned* flags) {
+    return guarded([&] {
+        require(st != nullptr, QRT_ERR_INVALID, "null state");
+        if (n_gates == 0) return;
+        require(arity && pos, QRT_ERR_INVALID, "null gate arrays");
+        require(mats != nullptr, QRT_ERR_MISSING_PAYLOAD, "gate payloads missing");
+        DeviceGuard g(st->device);
+        st->stats[QRT_K_GATES].calls++;
+        apply_gates(st, n_gates, arity, pos, mats, flags);
+        QRT_CUDA(cudaStreamSynchronize(st->stream));
+    });
+}
+
+qrt_status qrt_reorder(qrt_state* st, const int* dest, std::uint64_t* relocated) {
+    return guarded([&] {
+        require(st && dest, QRT_ERR_INVALID, "null argument");
+        DeviceGuard g(st->device);
+        st->stats[QRT_K_QR].calls++;
+        std::uint64_t moved = reorder(st, dest);
+        QRT_CUDA(cudaStreamSynchronize(st->stream));
+        if (relocated) *relocated = moved;
+    });
+}
+
+qrt_status qrt_pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const std::uint64_t* y,
+                                 const std::uint64_t* z, const std::uint64_t* gz, const double* coeffs,
+                                 double* partial) {
+    return guarded([&] {
+        require(st && partial, QRT_ERR_INVALID, "null argument");
+        require(n_terms == 0 || (x && y && z && gz && coeffs), QRT_ERR_INVALID, "null term arrays");
+        DeviceGuard g(st->device);
+        st->stats[QRT_K_PAULI].calls++;
+        pauli_expectation(st, n_terms, x, y, z, gz, coeffs, partial);
+    });
+}
+
+qrt_status qrt_norm(qrt_state* st, double* out) {
+    return guarded([&] {
+        require(st && out, QRT_ERR_INVALID, "null argument");
+        DeviceGuard g(st->device);
+        *out = norm(st);
+    });
+}
+
+qrt_status qrt_profile_enable(qrt_state* st, int on) {
+    return guarded([&] {
+        require(st != nullptr, QRT_ERR_INVALID, "null state");
+        st->profile = on != 0;
+    });
+}
+
+qrt_status qrt_stats(const qrt_state* st, qrt_kernel_stats out[QRT_K_COUNT]) {
+    return guarded([&] {
+        require(st && out, QRT_ERR_INVALID, "null argument");
+        for (int i = 0; i < QRT_K_COUNT; ++i) out[i] = st->stats[i];
+    });
+}
+
+qrt_status qrt_stats_reset(qrt_state* st) {
+    return guarded([&] {
+        require(st != nullptr, QRT_ERR_INVALID, "null state");
+        for (auto& s : st->stats) s = qrt_kernel_stats{};
+    });
+}
+
+qrt_status qrt_state_stream(const qrt_state* st, void** stream) {
+    return guarded([&] {
+        require(st && stream, QRT_ERR_INVALID, "null argument");
+        *stream = st->stream;
+    });
+}
+
+qrt_status qrt_synchronize(qrt_state* st) {
+    return guarded([&] {
+        require(st != nullptr, QRT_ERR_INVALID, "null state");
+        DeviceGuard g(st->device);
+        QRT_CUDA(cudaStreamSynchronize(st->stream));
+    });
+}
+
+}  // extern "C"

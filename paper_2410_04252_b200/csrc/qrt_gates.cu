@@ -1,0 +1,532 @@
+// libqrt — QSU gate runs (reference apply_gate_narrow, dist_sim.cpp:163-201).
+//
+// A call carries a sequence of narrow gates.  The host planner cuts it into
+// *passes*: each pass picks a set B of kTileBits local positions (always
+// containing the kCoalBits lowest positions, so every HBM access is a
+// contiguous run of 2^kCoalBits amplitudes) and takes, in order, every gate
+// whose targets lie in B (diagonal gates may target any position) without
+// overtaking a deferred gate on a shared qubit — the reference's own tile
+// construction (qsu_scheduler.cpp:37-60), re-applied at SM level.
+//
+// One pass = one kernel = one HBM round trip: each CTA loads the 2^12
+// amplitudes that agree on all positions outside B into shared memory
+// (XOR-swizzled against bank conflicts), applies the pass's gates in order
+// with fp64 FMAs (matrices staged in shared memory, broadcast reads), and
+// writes the tile back.  Algorithmic traffic per pass = 32 B x 2^(n-g);
+// flops per dense k-qubit gate = 8 x 2^k x 2^(n-g).
+
+#include <algorithm>
+#include <cstring>
+
+#include "qrt_internal.h"
+
+namespace qrt {
+
+namespace {
+
+constexpr int kDense = 0, kDiag = 1;
+constexpr int kMaxDiagK = 8;
+constexpr int kBigK = 16;  // cap for the out-of-place generic kernel
+
+struct PePtrs {
+    amp_t* p[kMaxLocalPEs];
+};
+
+struct GateOp {
+    int kind;
+    int k;
+    int smat;          // offset of the matrix / diagonal in the pass's smem stage, -1 if read from global
+    int gmat;          // offset into the call's matrix pool (double2 units)
+    int tb[kMaxDiagK]; // tile-bit index of targets[j] (-1: outside the tile, diagonal only)
+    int pos[kMaxDiagK];// physical position of targets[j]
+};
+
+struct PassHdr {
+    int T;               // tile bits
+    int c;               // leading tile bits that are exactly positions 0..c-1
+    int n_ops;
+    int op_begin;
+    int mat_begin;       // first double2 of this pass's staged matrices in the pool
+    int mat_count;
+    int n_outer;
+    int tile_pos[kTileBits];
+    int outer_pos[64];
+};
+
+__device__ __forceinline__ int swz(int e) {
+    int x = e >> 3;
+    return e ^ ((x ^ (x >> 3) ^ (x >> 6) ^ (x >> 9)) & 7);
+}
+
+__device__ __forceinline__ void cfma(double2& acc, const double2 u, const double2 a) {
+    acc.x = fma(u.x, a.x, acc.x);
+    acc.x = fma(-u.y, a.y, acc.x);
+    acc.y = fma(u.x, a.y, acc.y);
+    acc.y = fma(u.y, a.x, acc.y);
+}
+
+__device__ __forceinline__ int insert_zero(int v, int bit) {
+    return ((v >> bit) << (bit + 1)) | (v & ((1 << bit) - 1));
+}
+
+// Dense k <= 4: one thread owns a whole group of 2^K amplitudes in registers.
+template <int K>
+__device__ __forceinline__ void dense_small(double2* __restrict__ tile, const double2* __restrict__ u,
+                                            const GateOp* __restrict__ op, int E) {
+    constexpr int D = 1 << K;
+    int tb[K], sb[K];
+    int offm[D];
+#pragma unroll
+    for (int j = 0; j < K; ++j) sb[j] = tb[j] = op->tb[j];
+    // ascending tile bits for zero insertion
+#pragma unroll
+    for (int a = 1; a < K; ++a)
+#pragma unroll
+        for (int b = K - 1; b >= a; --b)
+            if (sb[b - 1] > sb[b]) {
+                int t = sb[b];
+                sb[b] = sb[b - 1];
+                sb[b - 1] = t;
+            }
+#pragma unroll
+    for (int m = 0; m < D; ++m) {
+        int o = 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) o |= ((m >> j) & 1) << tb[j];
+        offm[m] = o;
+    }
+    const int groups = E >> K;
+    for (int g = threadIdx.x; g < groups; g += blockDim.x) {
+        int base = g;
+#pragma unroll
+        for (int j = 0; j < K; ++j) base = insert_zero(base, sb[j]);
+        double2 a[D];
+#pragma unroll
+        for (int m = 0; m < D; ++m) a[m] = tile[swz(base | offm[m])];
+        // rows in pairs: two independent accumulators per thread, row
+        // offsets recomputed (keeps the unrolled matrix loads from hoisting)
+#pragma unroll 1
+        for (int r = 0; r < D; r += 2) {
+            double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+            const double2* u0 = u + r * D;
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                cfma(acc0, u0[c], a[c]);
+                if (D > 1) cfma(acc1, u0[D + c], a[c]);
+            }
+            int o0 = 0, o1 = 0;
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                o0 |= ((r >> j) & 1) << tb[j];
+                o1 |= (((r + 1) >> j) & 1) << tb[j];
+            }
+            tile[swz(base | o0)] = acc0;
+            tile[swz(base | o1)] = acc1;
+        }
+    }
+}
+
+// Dense 5 <= k <= 7: one warp per group, lanes split the rows.
+__device__ __noinline__ void dense_wide(double2* __restrict__ tile, const double2* __restrict__ u,
+                                        const GateOp* __restrict__ op, int E) {
+    const int K = op->k, D = 1 << K, per = D >> 5;
+    // zero-insertion in ascending bit order: repeatedly pick the smallest
+    // target bit above the previous one
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int groups = E >> K;
+    for (int g = warp; g < groups; g += nwarps) {
+        int base = g, prev = -1;
+        for (int j = 0; j < K; ++j) {
+            int low = 64;
+            for (int q = 0; q < K; ++q) {
+                const int b = op->tb[q];
+                if (b > prev && b < low) low = b;
+            }
+            base = insert_zero(base, low);
+            prev = low;
+        }
+        double2 acc[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] = make_double2(0.0, 0.0);
+        for (int c = 0; c < D; ++c) {
+            int oc = 0;
+            for (int j = 0; j < K; ++j) oc |= ((c >> j) & 1) << op->tb[j];
+            const double2 x = tile[swz(base | oc)];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (j < per) cfma(acc[j], u[(lane + 32 * j) * D + c], x);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (j >= per) continue;
+            const int r = lane + 32 * j;
+            int orow = 0;
+            for (int b = 0; b < K; ++b) orow |= ((r >> b) & 1) << op->tb[b];
+            tile[swz(base | orow)] = acc[j];
+        }
+        __syncwarp();
+    }
+}
+
+__device__ __noinline__ void diagonal(double2* __restrict__ tile, const double2* __restrict__ d,
+                                      const GateOp* __restrict__ op, int E, std::uint64_t base) {
+    const int k = op->k;
+    int fixed = 0, inmask = 0;
+    int tb[kMaxDiagK];
+#pragma unroll
+    for (int j = 0; j < kMaxDiagK; ++j) {
+        tb[j] = j < k ? op->tb[j] : -1;
+        if (j < k && tb[j] < 0) fixed |= static_cast<int>((base >> op->pos[j]) & 1ull) << j;
+        if (tb[j] >= 0) inmask |= 1 << j;
+    }
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        int m = fixed;
+#pragma unroll
+        for (int j = 0; j < kMaxDiagK; ++j)
+            if ((inmask >> j) & 1) m |= ((e >> tb[j]) & 1) << j;
+        const double2 w = d[m];
+        const int s = swz(e);
+        const double2 a = tile[s];
+        double2 r;
+        r.x = fma(w.x, a.x, -w.y * a.y);
+        r.y = fma(w.x, a.y, w.y * a.x);
+        tile[s] = r;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+    gate_pass_kernel(PePtrs ptrs, const PassHdr hdr, const GateOp* __restrict__ ops,
+                     const double2* __restrict__ pool) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int T = hdr.T, E = 1 << T, c = hdr.c;
+    double2* tile = reinterpret_cast<double2*>(smem_raw);
+    double2* smat = tile + E;
+    std::uint64_t* tab = reinterpret_cast<std::uint64_t*>(smat + hdr.mat_count);
+    const int nt = 1 << (T - c);
+
+    std::uint64_t base = 0;
+    {
+        const std::uint64_t b = blockIdx.x;
+        for (int i = 0; i < hdr.n_outer; ++i) base |= ((b >> i) & 1ull) << hdr.outer_pos[i];
+    }
+    for (int h = threadIdx.x; h < nt; h += blockDim.x) {
+        std::uint64_t o = 0;
+        for (int i = c; i < T; ++i) o |= static_cast<std::uint64_t>((h >> (i - c)) & 1) << hdr.tile_pos[i];
+        tab[h] = o;
+    }
+    for (int i = threadIdx.x; i < hdr.mat_count; i += blockDim.x) smat[i] = pool[hdr.mat_begin + i];
+    __syncthreads();
+
+    amp_t* __restrict__ v = ptrs.p[blockIdx.y];
+    const int cmask = (1 << c) - 1;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) tile[swz(e)] = __ldcs(&v[base | tab[e >> c] | (e & cmask)]);
+    __syncthreads();
+
+    for (int o = 0; o < hdr.n_ops; ++o) {
+        const GateOp* op = ops + hdr.op_begin + o;
+        const int smo = op->smat;
+        const double2* u = smo >= 0 ? smat + smo : pool + op->gmat;
+        if (op->kind == kDiag) {
+            diagonal(tile, u, op, E, base);
+        } else {
+            switch (op->k) {
+                case 1: dense_small<1>(tile, u, op, E); break;
+                case 2: dense_small<2>(tile, u, op, E); break;
+                case 3: dense_small<3>(tile, u, op, E); break;
+                case 4: dense_small<4>(tile, u, op, E); break;
+                default: dense_wide(tile, u, op, E); break;
+            }
+        }
+        __syncthreads();
+    }
+
+    for (int e = threadIdx.x; e < E; e += blockDim.x) __stcs(&v[base | tab[e >> c] | (e & cmask)], tile[swz(e)]);
+}
+
+// Out-of-place generic gate for very wide payloads: out[i] = sum_c U[row(i)][c] in[...].
+__global__ void wide_gate_kernel(const amp_t* __restrict__ in, amp_t* __restrict__ out, std::uint64_t amps,
+                                 const double2* __restrict__ u, int k, int diag, const int* __restrict__ posv) {
+    int pos[kBigK];
+    std::uint64_t tmask = 0;
+    for (int j = 0; j < k; ++j) {
+        pos[j] = posv[j];
+        tmask |= 1ull << pos[j];
+    }
+    const int D = 1 << k;
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < amps;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        int row = 0;
+        for (int j = 0; j < k; ++j) row |= static_cast<int>((i >> pos[j]) & 1ull) << j;
+        double2 acc = make_double2(0.0, 0.0);
+        if (diag) {
+            cfma(acc, u[row], in[i]);
+        } else {
+            const std::uint64_t cleared = i & ~tmask;
+            for (int cidx = 0; cidx < D; ++cidx) {
+                std::uint64_t src = cleared;
+                for (int j = 0; j < k; ++j) src |= static_cast<std::uint64_t>((cidx >> j) & 1) << pos[j];
+                cfma(acc, u[static_cast<std::size_t>(row) * D + cidx], in[src]);
+            }
+        }
+        out[i] = acc;
+    }
+}
+
+struct HostOp {
+    int kind, k;
+    int pos[kBigK];
+    std::uint64_t mask;
+    std::size_t mat_off;  // offset into the caller's mats (doubles)
+    int mat_len;          // double2 entries
+};
+
+}  // namespace
+
+void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, const double* mats,
+                 const unsigned* flags) {
+    const int nl = st->nl;
+    // ---- decode and validate -------------------------------------------------
+    std::vector<HostOp> opsv(static_cast<std::size_t>(n_gates));
+    std::size_t pcur = 0, mcur = 0;
+    for (int i = 0; i < n_gates; ++i) {
+        HostOp& h = opsv[static_cast<std::size_t>(i)];
+        h.k = arity[i];
+        if (h.k < 1 || h.k > nl) fail(QRT_ERR_ACCESS_VIOLATION, "gate arity out of range for the local region");
+        if (h.k > kBigK) fail(QRT_ERR_INVALID, "gate arity above the supported maximum of 16");
+        h.kind = (flags && (flags[i] & QRT_GATE_DIAGONAL)) ? kDiag : kDense;
+        h.mask = 0;
+        for (int j = 0; j < h.k; ++j) {
+            const int p = pos[pcur++];
+            if (p < 0 || p >= nl) fail(QRT_ERR_ACCESS_VIOLATION, "gate targets a global position; reorder first");
+            if (h.mask >> p & 1ull) fail(QRT_ERR_INVALID, "duplicate target position");
+            h.mask |= 1ull << p;
+            h.pos[j] = p;
+        }
+        h.mat_off = mcur;
+        h.mat_len = h.kind == kDiag ? (1 << h.k) : (1 << (2 * h.k));
+        mcur += static_cast<std::size_t>(2 * h.mat_len);
+    }
+
+    // ---- plan passes -----------------------------------------------------------
+    struct Pass {
+        bool wide = false;
+        int T = 0, c = 0;
+        std::vector<int> tile_pos;
+        std::vector<int> ops;
+    };
+    std::vector<Pass> passes;
+    std::vector<int> remaining(static_cast<std::size_t>(n_gates));
+    for (int i = 0; i < n_gates; ++i) remaining[static_cast<std::size_t>(i)] = i;
+    auto is_wide = [&](const HostOp& h) {
+        return h.kind == kDiag ? h.k > kMaxDiagK : h.k > kMaxTileGateK;
+    };
+    const bool whole = nl <= kTileBits;
+    while (!remaining.empty()) {
+        std::uint64_t B = 0;
+        if (whole) {
+            B = (nl >= 64) ? ~0ull : ((1ull << nl) - 1);
+        } else {
+            B = (1ull << kCoalBits) - 1;
+            std::uint64_t blocked = 0;
+            for (int id : remaining) {
+                const HostOp& h = opsv[static_cast<std::size_t>(id)];
+                if (h.kind == kDiag) {
+                    if (h.mask & blocked) blocked |= h.mask;
+                    continue;
+                }
+                if ((h.mask & blocked) || is_wide(h) || __builtin_popcountll(B | h.mask) > kTileBits) {
+                    blocked |= h.mask;
+                    continue;
+                }
+                B |= h.mask;
+                if (__builtin_popcountll(B) == kTileBits) break;
+            }
+            for (int p = 0; p < nl && __builtin_popcountll(B) < kTileBits; ++p) B |= 1ull << p;
+        }
+        Pass ps;
+        std::uint64_t blocked = 0;
+        int mat_used = 0;
+        std::vector<int> keep;
+        keep.reserve(remaining.size());
+        bool closed = false;
+        for (int id : remaining) {
+            const HostOp& h = opsv[static_cast<std::size_t>(id)];
+            if (closed || (h.mask & blocked)) {
+                blocked |= h.mask;
+                keep.push_back(id);
+                continue;
+            }
+            if (is_wide(h)) {
+                if (ps.ops.empty()) {  // runs alone, out of place
+                    ps.wide = true;
+                    ps.ops.push_back(id);
+                    closed = true;
+                } else {
+                    blocked |= h.mask;
+                    keep.push_back(id);
+                }
+                continue;
+            }
+            const bool fits = h.kind == kDiag || (h.mask & ~B) == 0;
+            const int staged = (h.kind == kDiag || h.k <= 4) ? h.mat_len : 0;
+            if (fits && mat_used + staged <= kMatBudget) {
+                ps.ops.push_back(id);
+                mat_used += staged;
+            } else {
+                blocked |= h.mask;
+                keep.push_back(id);
+            }
+        }
+        if (ps.ops.empty()) fail(QRT_ERR_INVALID, "gate planner made no progress");
+        if (!ps.wide) {
+            for (int p = 0; p < nl; ++p)
+                if (B >> p & 1ull) ps.tile_pos.push_back(p);
+            ps.T = static_cast<int>(ps.tile_pos.size());
+            ps.c = 0;
+            while (ps.c < ps.T && ps.tile_pos[static_cast<std::size_t>(ps.c)] == ps.c) ++ps.c;
+        }
+        passes.push_back(std::move(ps));
+        remaining.swap(keep);
+    }
+
+    // ---- pack descriptors + matrices into one upload ------------------------------
+    std::vector<GateOp> dev_ops;
+    std::vector<PassHdr> hdrs;
+    std::vector<double2> pool;
+    std::vector<int> wide_pos;  // for wide passes: positions (kBigK per pass)
+    for (Pass& ps : passes) {
+        PassHdr h{};
+        if (ps.wide) {
+            const HostOp& o = opsv[static_cast<std::size_t>(ps.ops[0])];
+            h.n_ops = 1;
+            h.op_begin = static_cast<int>(dev_ops.size());
+            h.mat_begin = static_cast<int>(pool.size());
+            h.mat_count = o.mat_len;
+            GateOp g{};
+            g.kind = o.kind;
+            g.k = o.k;
+            g.smat = -1;
+            g.gmat = h.mat_begin;
+            dev_ops.push_back(g);
+            for (int e = 0; e < o.mat_len; ++e)
+                pool.push_back(make_double2(mats[o.mat_off + 2 * static_cast<std::size_t>(e)],
+                                            mats[o.mat_off + 2 * static_cast<std::size_t>(e) + 1]));
+            h.T = -static_cast<int>(wide_pos.size()) - 1;  // marks a wide pass; index into wide_pos
+            for (int j = 0; j < kBigK; ++j) wide_pos.push_back(j < o.k ? o.pos[j] : 0);
+            hdrs.push_back(h);
+            continue;
+        }
+        h.T = ps.T;
+        h.c = ps.c;
+        h.n_ops = static_cast<int>(ps.ops.size());
+        h.op_begin = static_cast<int>(dev_ops.size());
+        h.mat_begin = static_cast<int>(pool.size());
+        for (int i = 0; i < ps.T; ++i) h.tile_pos[i] = ps.tile_pos[static_cast<std::size_t>(i)];
+        int no = 0;
+        std::uint64_t inB = 0;
+        for (int p : ps.tile_pos) inB |= 1ull << p;
+        for (int p = 0; p < nl; ++p)
+            if (!(inB >> p & 1ull)) h.outer_pos[no++] = p;
+        h.n_outer = no;
+        int tb_of[64];
+        for (int p = 0; p < 64; ++p) tb_of[p] = -1;
+        for (int i = 0; i < ps.T; ++i) tb_of[ps.tile_pos[static_cast<std::size_t>(i)]] = i;
+        // staged matrices first (contiguous), then global-only ones after
+        int staged = 0;
+        std::vector<std::pair<int, int>> late;  // (op index in dev_ops, host op)
+        for (int id : ps.ops) {
+            const HostOp& o = opsv[static_cast<std::size_t>(id)];
+            GateOp g{};
+            g.kind = o.kind;
+            g.k = o.k;
+            for (int j = 0; j < o.k; ++j) {
+                g.tb[j] = tb_of[o.pos[j]];
+                g.pos[j] = o.pos[j];
+            }
+            if (o.kind == kDiag || o.k <= 4) {
+                g.smat = staged;
+                g.gmat = h.mat_begin + staged;
+                for (int e = 0; e < o.mat_len; ++e)
+                    pool.push_back(make_double2(mats[o.mat_off + 2 * static_cast<std::size_t>(e)],
+                                                mats[o.mat_off + 2 * static_cast<std::size_t>(e) + 1]));
+                staged += o.mat_len;
+            } else {
+                g.smat = -1;
+                late.emplace_back(static_cast<int>(dev_ops.size()), id);
+            }
+            dev_ops.push_back(g);
+        }
+        h.mat_count = staged;
+        for (auto [di, id] : late) {
+            const HostOp& o = opsv[static_cast<std::size_t>(id)];
+            dev_ops[static_cast<std::size_t>(di)].gmat = static_cast<int>(pool.size());
+            for (int e = 0; e < o.mat_len; ++e)
+                pool.push_back(make_double2(mats[o.mat_off + 2 * static_cast<std::size_t>(e)],
+                                            mats[o.mat_off + 2 * static_cast<std::size_t>(e) + 1]));
+        }
+        hdrs.push_back(h);
+    }
+
+    const std::size_t ops_bytes = dev_ops.size() * sizeof(GateOp);
+    const std::size_t pool_off = (ops_bytes + 255) & ~std::size_t{255};
+    const std::size_t pool_bytes = pool.size() * sizeof(double2);
+    const std::size_t wpos_off = (pool_off + pool_bytes + 255) & ~std::size_t{255};
+    const std::size_t total = wpos_off + wide_pos.size() * sizeof(int) + 16;
+    char* host = static_cast<char*>(ensure_pinned(st, total));
+    QRT_CUDA(cudaStreamSynchronize(st->stream));  // pinned buffer may still feed a previous copy
+    std::memcpy(host, dev_ops.data(), ops_bytes);
+    std::memcpy(host + pool_off, pool.data(), pool_bytes);
+    std::memcpy(host + wpos_off, wide_pos.data(), wide_pos.size() * sizeof(int));
+    char* dev = static_cast<char*>(ensure_ops(st, total));
+    QRT_CUDA(cudaMemcpyAsync(dev, host, total, cudaMemcpyHostToDevice, st->stream));
+    const GateOp* d_ops = reinterpret_cast<const GateOp*>(dev);
+    const double2* d_pool = reinterpret_cast<const double2*>(dev + pool_off);
+    const int* d_wpos = reinterpret_cast<const int*>(dev + wpos_off);
+
+    static bool attr_done[64] = {};
+    if (!attr_done[st->device]) {
+        QRT_CUDA(cudaFuncSetAttribute(gate_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_done[st->device] = true;
+    }
+
+    PePtrs ptrs{};
+    ProfileScope prof(st, QRT_K_GATES);
+    const double amps_all = static_cast<double>(st->amps) * st->pe_count;
+    for (std::size_t pi = 0; pi < hdrs.size(); ++pi) {
+        const PassHdr& h = hdrs[pi];
+        if (h.T < 0) {  // wide, out of place into the alternate buffer, then copied back
+            ensure_alt(st);
+            const GateOp& g = dev_ops[static_cast<std::size_t>(h.op_begin)];
+            const int widx = -h.T - 1;
+            for (int i = 0; i < st->pe_count; ++i) {
+                amp_t* src = st->bufs[st->cur][static_cast<std::size_t>(i)];
+                amp_t* dst = st->bufs[st->cur ^ 1][static_cast<std::size_t>(i)];
+                wide_gate_kernel<<<148 * 8, 256, 0, st->stream>>>(src, dst, st->amps, d_pool + g.gmat, g.k,
+                                                                  g.kind == kDiag, d_wpos + widx);
+                QRT_CUDA(cudaGetLastError());
+                QRT_CUDA(cudaMemcpyAsync(src, dst, st->amps * sizeof(amp_t), cudaMemcpyDeviceToDevice, st->stream));
+            }
+            st->stats[QRT_K_GATES].launches += static_cast<std::uint64_t>(st->pe_count);
+            st->stats[QRT_K_GATES].bytes += 64.0 * amps_all;
+            st->stats[QRT_K_GATES].flops += 8.0 * (g.kind == kDiag ? 1.0 : static_cast<double>(1 << g.k)) * amps_all;
+            continue;
+        }
+        for (int i = 0; i < st->pe_count; ++i) ptrs.p[i] = st->live(i);
+        const int tiles = 1 << (st->nl - h.T);
+        const std::size_t smem = (static_cast<std::size_t>(1) << h.T) * sizeof(double2) +
+                                 static_cast<std::size_t>(h.mat_count) * sizeof(double2) +
+                                 (static_cast<std::size_t>(1) << (h.T - h.c)) * sizeof(std::uint64_t);
+        dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(st->pe_count));
+        gate_pass_kernel<<<grid, kThreads, smem, st->stream>>>(ptrs, h, d_ops, d_pool);
+        QRT_CUDA(cudaGetLastError());
+        st->stats[QRT_K_GATES].launches++;
+        st->stats[QRT_K_GATES].bytes += 32.0 * amps_all;
+        for (int o = 0; o < h.n_ops; ++o) {
+            const GateOp& g = dev_ops[static_cast<std::size_t>(h.op_begin + o)];
+            st->stats[QRT_K_GATES].flops += 8.0 * (g.kind == kDiag ? 1.0 : static_cast<double>(1 << g.k)) * amps_all;
+        }
+    }
+}
+
+}  // namespace qrt

@@ -1,0 +1,121 @@
+// Internal declarations of libqrt (the C ABI in include/qrt.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "qrt.h"
+
+namespace qrt {
+
+// Thrown inside the library, converted to a status + qrt_last_error() at the
+// ABI boundary.
+struct Failure : std::runtime_error {
+    qrt_status status;
+    Failure(qrt_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+[[noreturn]] void fail(qrt_status s, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+void nccl_check(ncclResult_t r, const char* what, const char* file, int line);
+#define QRT_CUDA(x) ::qrt::cuda_check((x), #x, __FILE__, __LINE__)
+#define QRT_NCCL(x) ::qrt::nccl_check((x), #x, __FILE__, __LINE__)
+
+using amp_t = double2;  // (re, im), 16 B, the HBM unit
+
+inline constexpr int kMaxLocalPEs = 64;  // PEs one process may own
+inline constexpr int kTileBits = 12;     // smem tile: 2^12 amplitudes = 64 KiB
+inline constexpr int kCoalBits = 4;      // low positions always inside a tile (256 B runs)
+inline constexpr int kMaxTileGateK = 7;  // dense gates up to 7 qubits run inside a tile
+inline constexpr int kMatBudget = 2048;  // max double2 matrix entries staged per pass (32 KiB)
+inline constexpr int kThreads = 256;
+
+}  // namespace qrt
+
+struct qrt_comm {
+    int rank = 0;
+    int world = 1;
+    int device = 0;
+    ncclComm_t nccl = nullptr;
+};
+
+struct KernelCounters {
+    qrt_kernel_stats s{};
+};
+
+struct qrt_state {
+    int n = 0;
+    int p = 1;
+    int nl = 0;  // local positions
+    int device = 0;
+    qrt_comm* comm = nullptr;
+    int pe_begin = 0;
+    int pe_count = 0;
+    std::uint64_t amps = 0;  // amplitudes per PE
+
+    // Two buffers per owned PE; `cur` selects the live one.  In multi-process
+    // mode both are allocated up front and IPC-shared; otherwise the second
+    // is allocated on first use (QR / out-of-place gate).
+    std::vector<qrt::amp_t*> bufs[2];
+    int cur = 0;
+    // Base pointer of every PE's buffers (all p PEs; remote ones IPC-mapped).
+    std::vector<qrt::amp_t*> peer[2];
+    std::vector<void*> ipc_opened;  // pointers to close on destroy
+
+    cudaStream_t stream = nullptr;
+
+    // Scratch: per-CTA reduction slots and small uploads.
+    double* d_red = nullptr;
+    std::size_t red_cap = 0;
+    void* d_ops = nullptr;  // op/pass descriptors + matrices of the current call
+    std::size_t ops_cap = 0;
+    void* h_pinned = nullptr;  // pinned staging for descriptor uploads
+    std::size_t pinned_cap = 0;
+    int* d_flag = nullptr;  // barrier word for NCCL
+
+    // Measurement.
+    bool profile = false;
+    qrt_kernel_stats stats[QRT_K_COUNT]{};
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    qrt::amp_t* live(int local_pe) const { return bufs[cur][static_cast<std::size_t>(local_pe)]; }
+};
+
+namespace qrt {
+
+// Scoped profiling region: records events around the launches of one kernel
+// family on the state's stream when profiling is on.
+struct ProfileScope {
+    qrt_state* st;
+    int fam;
+    ProfileScope(qrt_state* s, int f);
+    ~ProfileScope() noexcept(false);
+};
+
+void ensure_alt(qrt_state* st);
+void* ensure_ops(qrt_state* st, std::size_t bytes);
+void* ensure_pinned(qrt_state* st, std::size_t bytes);
+double* ensure_red(qrt_state* st, std::size_t doubles);
+void barrier_on_stream(qrt_state* st);  // NCCL all-reduce of one int (no-op single process)
+
+// Families implemented in the .cu files.
+void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, const double* mats,
+                 const unsigned* flags);
+std::uint64_t reorder(qrt_state* st, const int* dest);
+void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const std::uint64_t* y,
+                       const std::uint64_t* z, const std::uint64_t* gz, const double* coeffs, double* partial);
+double norm(qrt_state* st);
+
+// Host helpers shared by planners.
+inline std::uint64_t deposit_bits(std::uint64_t value, const int* positions, int count) {
+    std::uint64_t out = 0;
+    for (int i = 0; i < count; ++i) out |= ((value >> i) & 1ull) << positions[i];
+    return out;
+}
+
+}  // namespace qrt

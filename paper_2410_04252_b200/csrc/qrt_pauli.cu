@@ -1,0 +1,421 @@
+// libqrt — expectation value computation for one EVC plan tile
+// (reference local_pauli_expectation + expectation, dist_sim.cpp:84-97 and
+// :289-298) and the state norm (:115-120).
+//
+// Terms are batched by their X|Y flip mask.  For a flip mask x != 0 the pair
+// (i, i^x) contributes  s(i) [w + (-1)^{#Y} conj(w)],  w = conj(v[i^x]) v[i],
+// so only the canonical half of the pairs is visited and only Re(w) or Im(w)
+// is needed: the X/Y flip and the Z/Y phase are applied in registers.  Terms
+// with x = 0 (I/Z words) are evaluated from a Walsh-Hadamard transform of
+// |v|^2 over the tile, so their cost per CTA is O(1) per term.
+//
+// A pass loads a 2^12-amplitude tile (positions B, chosen so the flip masks of
+// many groups lie inside B) into shared memory once and evaluates every group
+// it covers; per-CTA partial sums are reduced in a fixed order (warp shuffle
+// -> block -> deterministic tree per PE), so results are run-to-run
+// identical.  Algorithmic traffic per pass = 16 B x 2^(n-g) read.
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+
+#include "qrt_internal.h"
+
+namespace qrt {
+
+namespace {
+
+struct PePtrsP {
+    const amp_t* p[kMaxLocalPEs];
+};
+
+struct PTerm {
+    std::uint64_t m;   // sign mask (z|y) over local positions
+    std::uint64_t gz;  // PE-index sign mask
+    double2 f;         // folded coefficient (x2 and i^#Y for flip terms)
+    int m_tile;        // m restricted to the tile, in tile-bit indices
+    int comp;          // 0: Re(w), 1: Im(w)
+};
+
+struct PGroup {
+    int xy_tile;
+    int hbit;
+    int t_begin;
+    int t_count;
+};
+
+struct PPass {
+    int T, c, n_outer;
+    int tile_pos[kTileBits];
+    int outer_pos[64];
+    int g_begin, g_count;
+    int d_begin, d_count;
+    int pe_begin;
+};
+
+__device__ __forceinline__ int swz(int e) {
+    int x = e >> 3;
+    return e ^ ((x ^ (x >> 3) ^ (x >> 6) ^ (x >> 9)) & 7);
+}
+__device__ __forceinline__ int insert_zero(int v, int bit) {
+    return ((v >> bit) << (bit + 1)) | (v & ((1 << bit) - 1));
+}
+__device__ __forceinline__ double flip_if(double v, int odd) { return odd ? -v : v; }
+
+__device__ __forceinline__ double2 block_sum(double2 v, double2* scratch) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v.x += __shfl_down_sync(0xffffffffu, v.x, o);
+        v.y += __shfl_down_sync(0xffffffffu, v.y, o);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    double2 r = make_double2(0.0, 0.0);
+    if (threadIdx.x == 0)
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            r.x += scratch[w].x;
+            r.y += scratch[w].y;
+        }
+    return r;
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+    pauli_pass_kernel(PePtrsP ptrs, const PPass P, const PGroup* __restrict__ groups, const PTerm* __restrict__ terms,
+                      double* __restrict__ red) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double2 scratch[kThreads / 32];
+    const int T = P.T, E = 1 << T, c = P.c;
+    double2* tile = reinterpret_cast<double2*>(smem_raw);
+    std::uint64_t* tab = reinterpret_cast<std::uint64_t*>(tile + E);
+    double* W = reinterpret_cast<double*>(tab + (1 << (T - c)));
+
+    std::uint64_t base = 0;
+    for (int i = 0; i < P.n_outer; ++i) base |= ((static_cast<std::uint64_t>(blockIdx.x) >> i) & 1ull) << P.outer_pos[i];
+    for (int h = threadIdx.x; h < (1 << (T - c)); h += blockDim.x) {
+        std::uint64_t o = 0;
+        for (int i = c; i < T; ++i) o |= static_cast<std::uint64_t>((h >> (i - c)) & 1) << P.tile_pos[i];
+        tab[h] = o;
+    }
+    __syncthreads();
+    const amp_t* __restrict__ v = ptrs.p[blockIdx.y];
+    const std::uint64_t pe = static_cast<std::uint64_t>(P.pe_begin) + blockIdx.y;
+    const int cmask = (1 << c) - 1;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        const double2 a = __ldcs(&v[base | tab[e >> c] | (e & cmask)]);
+        tile[swz(e)] = a;
+        if (P.d_count > 0) W[e] = fma(a.x, a.x, a.y * a.y);
+    }
+    __syncthreads();
+
+    double2 acc = make_double2(0.0, 0.0);
+    if (P.d_count > 0) {  // diagonal words: WHT of |v|^2 over the tile
+        for (int s = 0; s < T; ++s) {
+            for (int i = threadIdx.x; i < (E >> 1); i += blockDim.x) {
+                const int i0 = insert_zero(i, s), i1 = i0 | (1 << s);
+                const double a = W[i0], b = W[i1];
+                W[i0] = a + b;
+                W[i1] = a - b;
+            }
+            __syncthreads();
+        }
+        for (int t = threadIdx.x; t < P.d_count; t += blockDim.x) {
+            const PTerm tm = terms[P.d_begin + t];
+            const int odd = (__popcll(base & tm.m) + __popcll(pe & tm.gz)) & 1;
+            const double val = flip_if(W[tm.m_tile], odd);
+            acc.x = fma(tm.f.x, val, acc.x);
+            acc.y = fma(tm.f.y, val, acc.y);
+        }
+    }
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int half = E >> 1;
+    for (int gi = warp; gi < P.g_count; gi += nwarps) {
+        const PGroup G = groups[P.g_begin + gi];
+        for (int t0 = 0; t0 < G.t_count; t0 += 4) {
+            const int nt = min(4, G.t_count - t0);
+            double2 F[4];
+            int mt[4], cp[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (q < nt) {
+                    const PTerm tm = terms[G.t_begin + t0 + q];
+                    const int odd = (__popcll(base & tm.m) + __popcll(pe & tm.gz)) & 1;
+                    F[q] = make_double2(flip_if(tm.f.x, odd), flip_if(tm.f.y, odd));
+                    mt[q] = tm.m_tile;
+                    cp[q] = tm.comp;
+                } else {
+                    F[q] = make_double2(0.0, 0.0);
+                    mt[q] = 0;
+                    cp[q] = 0;
+                }
+            }
+            for (int idx = lane; idx < half; idx += 32) {
+                const int e = insert_zero(idx, G.hbit);
+                const double2 a = tile[swz(e ^ G.xy_tile)];
+                const double2 b = tile[swz(e)];
+                const double re = fma(a.x, b.x, a.y * b.y);
+                const double im = fma(a.x, b.y, -a.y * b.x);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (q < nt) {
+                        const double val = flip_if(cp[q] ? im : re, __popc(e & mt[q]) & 1);
+                        acc.x = fma(F[q].x, val, acc.x);
+                        acc.y = fma(F[q].y, val, acc.y);
+                    }
+                }
+            }
+        }
+    }
+    const double2 tot = block_sum(acc, scratch);
+    if (threadIdx.x == 0) {
+        double* slot = red + 2 * (static_cast<std::size_t>(blockIdx.y) * gridDim.x + blockIdx.x);
+        slot[0] += tot.x;
+        slot[1] += tot.y;
+    }
+}
+
+// Deterministic per-PE reduction of `count` slots of (re, im).
+__global__ void __launch_bounds__(256) reduce_slots_kernel(const double* __restrict__ red, int count, double* out) {
+    __shared__ double2 scratch[8];
+    const double* r = red + 2 * static_cast<std::size_t>(blockIdx.x) * count;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int i = threadIdx.x; i < count; i += blockDim.x) {
+        acc.x += r[2 * i];
+        acc.y += r[2 * i + 1];
+    }
+    const double2 tot = block_sum(acc, scratch);
+    if (threadIdx.x == 0) {
+        out[2 * blockIdx.x] = tot.x;
+        out[2 * blockIdx.x + 1] = tot.y;
+    }
+}
+
+__global__ void __launch_bounds__(256) norm_kernel(const amp_t* __restrict__ v, std::uint64_t amps, double* red) {
+    __shared__ double2 scratch[8];
+    double2 acc = make_double2(0.0, 0.0);
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < amps;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const double2 a = __ldcs(&v[i]);
+        acc.x = fma(a.x, a.x, fma(a.y, a.y, acc.x));
+    }
+    const double2 tot = block_sum(acc, scratch);
+    if (threadIdx.x == 0) {
+        red[2 * blockIdx.x] = tot.x;
+        red[2 * blockIdx.x + 1] = 0.0;
+    }
+}
+
+int popc(std::uint64_t v) { return __builtin_popcountll(v); }
+
+// Gathers `local` (2 doubles per owned PE) into `all` (2 doubles per PE).
+void gather_partials(qrt_state* st, const double* d_local, double* all) {
+    const std::size_t per = 2 * static_cast<std::size_t>(st->pe_count);
+    if (st->comm && st->comm->world > 1) {
+        double* buf = nullptr;
+        QRT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), 2 * static_cast<std::size_t>(st->p) * sizeof(double),
+                                 st->stream));
+        QRT_NCCL(ncclAllGather(d_local, buf, per, ncclDouble, st->comm->nccl, st->stream));
+        QRT_CUDA(cudaMemcpyAsync(all, buf, 2 * static_cast<std::size_t>(st->p) * sizeof(double), cudaMemcpyDeviceToHost,
+                                 st->stream));
+        QRT_CUDA(cudaFreeAsync(buf, st->stream));
+        QRT_CUDA(cudaStreamSynchronize(st->stream));
+    } else {
+        QRT_CUDA(cudaMemcpyAsync(all + 2 * static_cast<std::size_t>(st->pe_begin), d_local, per * sizeof(double),
+                                 cudaMemcpyDeviceToHost, st->stream));
+        QRT_CUDA(cudaStreamSynchronize(st->stream));
+    }
+}
+
+}  // namespace
+
+void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const std::uint64_t* y,
+                       const std::uint64_t* z, const std::uint64_t* gz, const double* coeffs, double* partial) {
+    const int nl = st->nl;
+    const std::uint64_t local_mask = nl >= 64 ? ~0ull : ((1ull << nl) - 1);
+    const std::uint64_t pe_mask = (st->p == 1) ? 0ull : static_cast<std::uint64_t>(st->p - 1);
+    for (int t = 0; t < n_terms; ++t) {
+        if ((x[t] | y[t] | z[t]) & ~local_mask) fail(QRT_ERR_INVALID, "term mask outside the local positions");
+        if ((x[t] & y[t]) || (x[t] & z[t]) || (y[t] & z[t])) fail(QRT_ERR_INVALID, "overlapping X/Y/Z masks");
+        if (gz[t] & ~pe_mask) fail(QRT_ERR_INVALID, "global Z mask outside the PE index");
+    }
+    for (int i = 0; i < 2 * st->p; ++i) partial[i] = 0.0;
+    if (n_terms == 0) return;
+
+    // ---- group by flip mask ------------------------------------------------
+    std::map<std::uint64_t, std::vector<int>> by_xy;
+    for (int t = 0; t < n_terms; ++t) by_xy[x[t] | y[t]].push_back(t);
+    std::vector<int> diag;
+    std::vector<std::pair<std::uint64_t, std::vector<int>>> flips;
+    for (auto& kv : by_xy) {
+        if (kv.first == 0)
+            diag = kv.second;
+        else
+            flips.emplace_back(kv.first, kv.second);
+    }
+
+    // ---- passes: choose tile positions covering many flip masks -------------
+    const int T = std::min(kTileBits, nl);
+    const int coal = std::min(kCoalBits, nl);
+    struct Pass {
+        std::uint64_t B;
+        std::vector<int> groups;  // indices into flips
+        bool has_diag;
+    };
+    std::vector<Pass> passes;
+    std::vector<int> left(flips.size());
+    for (std::size_t i = 0; i < flips.size(); ++i) left[i] = static_cast<int>(i);
+    // widest masks first so they seed the tiles
+    std::stable_sort(left.begin(), left.end(), [&](int a, int b) {
+        return popc(flips[static_cast<std::size_t>(a)].first) > popc(flips[static_cast<std::size_t>(b)].first);
+    });
+    bool diag_done = diag.empty();
+    while (!left.empty() || !diag_done) {
+        std::uint64_t B = (coal >= 64) ? ~0ull : ((1ull << coal) - 1);
+        if (T == nl) {
+            B = local_mask;
+        } else {
+            for (int gi : left) {
+                const std::uint64_t m = flips[static_cast<std::size_t>(gi)].first;
+                if (popc(B | m) <= T) B |= m;
+                if (popc(B) == T) break;
+            }
+            for (int p = 0; p < nl && popc(B) < T; ++p) B |= 1ull << p;
+        }
+        Pass ps{B, {}, !diag_done};
+        diag_done = true;
+        std::vector<int> keep;
+        for (int gi : left)
+            ((flips[static_cast<std::size_t>(gi)].first & ~B) == 0 ? ps.groups : keep).push_back(gi);
+        if (ps.groups.empty() && !ps.has_diag) fail(QRT_ERR_INVALID, "EVC planner made no progress");
+        passes.push_back(std::move(ps));
+        left.swap(keep);
+    }
+
+    // ---- device descriptors --------------------------------------------------
+    std::vector<PGroup> dgroups;
+    std::vector<PTerm> dterms;
+    std::vector<PPass> hdrs;
+    auto compress = [](std::uint64_t m, const int* tile_pos, int Tn) {
+        int r = 0;
+        for (int i = 0; i < Tn; ++i) r |= static_cast<int>((m >> tile_pos[i]) & 1ull) << i;
+        return r;
+    };
+    for (const Pass& ps : passes) {
+        PPass h{};
+        h.T = T;
+        h.pe_begin = st->pe_begin;
+        int ti = 0, no = 0;
+        for (int p = 0; p < nl; ++p) {
+            if (ps.B >> p & 1ull)
+                h.tile_pos[ti++] = p;
+            else
+                h.outer_pos[no++] = p;
+        }
+        h.n_outer = no;
+        h.c = 0;
+        while (h.c < T && h.tile_pos[h.c] == h.c) ++h.c;
+        h.d_begin = static_cast<int>(dterms.size());
+        h.d_count = 0;
+        if (ps.has_diag) {
+            for (int t : diag) {
+                PTerm tm{};
+                tm.m = z[t] | y[t];
+                tm.gz = gz[t];
+                tm.f = make_double2(coeffs[2 * t], coeffs[2 * t + 1]);
+                tm.m_tile = compress(tm.m & ps.B, h.tile_pos, T);
+                tm.comp = 0;
+                dterms.push_back(tm);
+            }
+            h.d_count = static_cast<int>(diag.size());
+        }
+        h.g_begin = static_cast<int>(dgroups.size());
+        h.g_count = static_cast<int>(ps.groups.size());
+        for (int gi : ps.groups) {
+            const auto& [xy, members] = flips[static_cast<std::size_t>(gi)];
+            PGroup G{};
+            G.xy_tile = compress(xy, h.tile_pos, T);
+            G.hbit = 31 - __builtin_clz(static_cast<unsigned>(G.xy_tile));
+            G.t_begin = static_cast<int>(dterms.size());
+            G.t_count = static_cast<int>(members.size());
+            for (int t : members) {
+                const int ycnt = popc(y[t]);
+                const double sgn = ((ycnt & 3) == 1 || (ycnt & 3) == 2) ? -2.0 : 2.0;
+                PTerm tm{};
+                tm.m = z[t] | y[t];
+                tm.gz = gz[t];
+                tm.f = make_double2(sgn * coeffs[2 * t], sgn * coeffs[2 * t + 1]);
+                tm.m_tile = compress(tm.m & ps.B, h.tile_pos, T);
+                tm.comp = ycnt & 1;
+                dterms.push_back(tm);
+            }
+            dgroups.push_back(G);
+        }
+        hdrs.push_back(h);
+    }
+    const std::size_t gbytes = dgroups.size() * sizeof(PGroup);
+    const std::size_t toff = (gbytes + 255) & ~std::size_t{255};
+    const std::size_t total = toff + dterms.size() * sizeof(PTerm) + 16;
+    char* host = static_cast<char*>(ensure_pinned(st, total));
+    QRT_CUDA(cudaStreamSynchronize(st->stream));
+    std::memcpy(host, dgroups.data(), gbytes);
+    std::memcpy(host + toff, dterms.data(), dterms.size() * sizeof(PTerm));
+    char* dev = static_cast<char*>(ensure_ops(st, total));
+    QRT_CUDA(cudaMemcpyAsync(dev, host, total, cudaMemcpyHostToDevice, st->stream));
+
+    const int ctas = 1 << (nl - T);
+    const std::size_t slots = static_cast<std::size_t>(ctas) * static_cast<std::size_t>(st->pe_count);
+    double* red = ensure_red(st, 2 * slots + 2 * static_cast<std::size_t>(st->pe_count));
+    double* out = red + 2 * slots;
+    QRT_CUDA(cudaMemsetAsync(red, 0, 2 * slots * sizeof(double), st->stream));
+
+    static bool attr_done[64] = {};
+    if (!attr_done[st->device]) {
+        QRT_CUDA(cudaFuncSetAttribute(pauli_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_done[st->device] = true;
+    }
+    PePtrsP ptrs{};
+    for (int i = 0; i < st->pe_count; ++i) ptrs.p[i] = st->live(i);
+    {
+        ProfileScope prof(st, QRT_K_PAULI);
+        for (const PPass& h : hdrs) {
+            const std::size_t smem = (std::size_t{1} << T) * sizeof(double2) +
+                                     (std::size_t{1} << (T - h.c)) * sizeof(std::uint64_t) +
+                                     (h.d_count > 0 ? (std::size_t{1} << T) * sizeof(double) : 0);
+            dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(st->pe_count));
+            pauli_pass_kernel<<<grid, kThreads, smem, st->stream>>>(
+                ptrs, h, reinterpret_cast<const PGroup*>(dev), reinterpret_cast<const PTerm*>(dev + toff), red);
+            QRT_CUDA(cudaGetLastError());
+            st->stats[QRT_K_PAULI].launches++;
+            st->stats[QRT_K_PAULI].bytes += 16.0 * static_cast<double>(st->amps) * st->pe_count;
+        }
+        reduce_slots_kernel<<<st->pe_count, 256, 0, st->stream>>>(red, ctas, out);
+        QRT_CUDA(cudaGetLastError());
+        st->stats[QRT_K_MISC].launches++;
+    }
+    // algorithmic flops: one complex MAC per amplitude per term (reference loop)
+    st->stats[QRT_K_PAULI].flops += 8.0 * static_cast<double>(st->amps) * st->pe_count * n_terms;
+    gather_partials(st, out, partial);
+}
+
+double norm(qrt_state* st) {
+    const int blocks = 148 * 4;
+    const std::size_t slots = static_cast<std::size_t>(blocks) * static_cast<std::size_t>(st->pe_count);
+    double* red = ensure_red(st, 2 * slots + 2 * static_cast<std::size_t>(st->pe_count));
+    double* out = red + 2 * slots;
+    for (int i = 0; i < st->pe_count; ++i) {
+        norm_kernel<<<blocks, 256, 0, st->stream>>>(st->live(i), st->amps, red + 2 * static_cast<std::size_t>(i) * blocks);
+        QRT_CUDA(cudaGetLastError());
+    }
+    reduce_slots_kernel<<<st->pe_count, 256, 0, st->stream>>>(red, blocks, out);
+    QRT_CUDA(cudaGetLastError());
+    st->stats[QRT_K_MISC].launches += static_cast<std::uint64_t>(st->pe_count) + 1;
+    std::vector<double> all(2 * static_cast<std::size_t>(st->p), 0.0);
+    gather_partials(st, out, all.data());
+    double s = 0.0;
+    for (int pe = 0; pe < st->p; ++pe) s += all[2 * static_cast<std::size_t>(pe)];
+    return std::sqrt(s);
+}
+
+}  // namespace qrt

@@ -11,7 +11,8 @@
 // One pass = one kernel = one HBM round trip: each CTA loads the 2^12
 // amplitudes that agree on all positions outside B into shared memory
 // (XOR-swizzled against bank conflicts), applies the pass's gates in order
-// with fp64 FMAs (matrices staged in shared memory, broadcast reads), and
+// with fp64 FMAs (dense matrices read from the launch parameters through the
+// uniform constant path, diagonals from shared memory), and
 // writes the tile back.  Algorithmic traffic per pass = 32 B x 2^(n-g);
 // flops per dense k-qubit gate = 8 x 2^k x 2^(n-g).
 
@@ -35,8 +36,10 @@ struct PePtrs {
 struct GateOp {
     int kind;
     int k;
-    int smat;          // offset of the matrix / diagonal in the pass's smem stage, -1 if read from global
-    int gmat;          // offset into the call's matrix pool (double2 units)
+    int smat;          // diagonal gates: offset of the diagonal in the pass's smem stage
+    int pmat;          // dense k<=4 gates: offset of the matrix in the launch parameters
+    int gmat;          // offset into the call's matrix pool in global memory (double2 units)
+    int bfrag;         // k=3,4 dense gates: offset of the DMMA B fragments (doubles), -1 if unused
     int tb[kMaxDiagK]; // tile-bit index of targets[j] (-1: outside the tile, diagonal only)
     int pos[kMaxDiagK];// physical position of targets[j]
 };
@@ -51,6 +54,21 @@ struct PassHdr {
     int n_outer;
     int tile_pos[kTileBits];
     int outer_pos[64];
+};
+
+// Dense k<=4 matrices travel inside the launch parameters (constant bank):
+// every thread of a warp reads the same entry at the same time, so the loads
+// go through the uniform/constant path instead of shared memory, whose
+// register write-back was the bottleneck (ncu: lsu_writeback 80%, fp64 32%).
+constexpr int kParamMats = 1664;  // double2 entries, 26 KiB (all params <= 32 KiB)
+constexpr int kMaxPassOps = 40;   // op descriptors per pass, also in the parameters
+constexpr int kDiagStage = 1024; // diagonal entries staged in smem per pass
+
+struct PassParams {
+    PePtrs ptrs;
+    PassHdr hdr;
+    GateOp ops[kMaxPassOps];
+    double2 mats[kParamMats];
 };
 
 __device__ __forceinline__ int swz(int e) {
@@ -71,13 +89,13 @@ __device__ __forceinline__ int insert_zero(int v, int bit) {
 
 // Dense k <= 4: one thread owns a whole group of 2^K amplitudes in registers.
 template <int K>
-__device__ __forceinline__ void dense_small(double2* __restrict__ tile, const double2* __restrict__ u,
-                                            const GateOp* __restrict__ op, int E) {
+__device__ __forceinline__ void dense_small(double2* __restrict__ tile, const PassParams& P, int moff,
+                                            const GateOp& op, int E) {
     constexpr int D = 1 << K;
     int tb[K], sb[K];
     int offm[D];
 #pragma unroll
-    for (int j = 0; j < K; ++j) sb[j] = tb[j] = op->tb[j];
+    for (int j = 0; j < K; ++j) sb[j] = tb[j] = op.tb[j];
     // ascending tile bits for zero insertion
 #pragma unroll
     for (int a = 1; a < K; ++a)
@@ -108,11 +126,11 @@ __device__ __forceinline__ void dense_small(double2* __restrict__ tile, const do
 #pragma unroll 1
         for (int r = 0; r < D; r += 2) {
             double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
-            const double2* u0 = u + r * D;
+            const int row = moff + r * D;
 #pragma unroll
             for (int c = 0; c < D; ++c) {
-                cfma(acc0, u0[c], a[c]);
-                if (D > 1) cfma(acc1, u0[D + c], a[c]);
+                cfma(acc0, P.mats[row + c], a[c]);
+                cfma(acc1, P.mats[row + D + c], a[c]);
             }
             int o0 = 0, o1 = 0;
 #pragma unroll
@@ -126,10 +144,90 @@ __device__ __forceinline__ void dense_small(double2* __restrict__ tile, const do
     }
 }
 
+// 16-byte global -> shared copy that bypasses registers (LDGSTS), so every
+// thread keeps all of its tile loads in flight at once.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// Dense k = 3, 4 on the FP64 tensor path (DMMA, m8n8k4): for 8 groups at a
+// time, OUT[8 x 2D] = IN[8 x 2D] * M^T where M is the 2D x 2D real form of U
+// ([[Re, -Im], [Im, Re]] blocks) — the interleaved (re, im) amplitude layout
+// is already the real vector.  B fragments (M^T) stay in registers for the
+// whole gate; each lane loads one double of A per k-block and stores one
+// complex output per n-block.  Fragment layout (PTX m8n8k4.f64):
+//   A: row = lane>>2, col = lane&3;  B: row = lane&3, col = lane>>2;
+//   C: row = lane>>2, cols 2*(lane&3) + {0,1}.
+template <int K>
+__device__ __forceinline__ void dense_dmma(double2* __restrict__ tile, const double* __restrict__ frag,
+                                           const GateOp& op, int E) {
+    constexpr int D = 1 << K, R = 2 * D, NB = R / 8, KB = R / 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    double b[NB][KB];
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) b[nb][kb] = __ldg(&frag[(nb * KB + kb) * 32 + lane]);
+    int tb[K], sb[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) sb[j] = tb[j] = op.tb[j];
+#pragma unroll
+    for (int a = 1; a < K; ++a)
+#pragma unroll
+        for (int q = K - 1; q >= a; --q)
+            if (sb[q - 1] > sb[q]) {
+                const int t = sb[q];
+                sb[q] = sb[q - 1];
+                sb[q - 1] = t;
+            }
+    auto spread = [&](int m) {
+        int o = 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) o |= ((m >> j) & 1) << tb[j];
+        return o;
+    };
+    // per-lane constant offsets: A columns (complex index 2kb + ((lane&3)>>1))
+    // and C rows (complex index 4nb + (lane&3))
+    int aoff[KB], coff[NB];
+#pragma unroll
+    for (int kb = 0; kb < KB; ++kb) aoff[kb] = spread(2 * kb + ((lane & 3) >> 1));
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) coff[nb] = spread(4 * nb + (lane & 3));
+    const int comp = lane & 1;
+    double* __restrict__ tiled = reinterpret_cast<double*>(tile);
+    const int blocks = (E >> K) >> 3;
+    for (int rb = warp; rb < blocks; rb += nwarps) {
+        int base = rb * 8 + (lane >> 2);
+#pragma unroll
+        for (int j = 0; j < K; ++j) base = insert_zero(base, sb[j]);
+        double a[KB];
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) a[kb] = tiled[2 * swz(base | aoff[kb]) + comp];
+        double acc[NB][2];
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) acc[nb][0] = acc[nb][1] = 0.0;
+        // k-blocks outer: the NB accumulator chains interleave
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb)
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) dmma_8x8x4(acc[nb][0], acc[nb][1], a[kb], b[nb][kb]);
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) tile[swz(base | coff[nb])] = make_double2(acc[nb][0], acc[nb][1]);
+    }
+}
+
 // Dense 5 <= k <= 7: one warp per group, lanes split the rows.
-__device__ __noinline__ void dense_wide(double2* __restrict__ tile, const double2* __restrict__ u,
-                                        const GateOp* __restrict__ op, int E) {
-    const int K = op->k, D = 1 << K, per = D >> 5;
+__device__ __forceinline__ void dense_wide(double2* __restrict__ tile, const double2* __restrict__ u,
+                                           const GateOp& op, int E) {
+    const int K = op.k, D = 1 << K, per = D >> 5;
     // zero-insertion in ascending bit order: repeatedly pick the smallest
     // target bit above the previous one
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -139,7 +237,7 @@ __device__ __noinline__ void dense_wide(double2* __restrict__ tile, const double
         for (int j = 0; j < K; ++j) {
             int low = 64;
             for (int q = 0; q < K; ++q) {
-                const int b = op->tb[q];
+                const int b = op.tb[q];
                 if (b > prev && b < low) low = b;
             }
             base = insert_zero(base, low);
@@ -150,7 +248,7 @@ __device__ __noinline__ void dense_wide(double2* __restrict__ tile, const double
         for (int j = 0; j < 4; ++j) acc[j] = make_double2(0.0, 0.0);
         for (int c = 0; c < D; ++c) {
             int oc = 0;
-            for (int j = 0; j < K; ++j) oc |= ((c >> j) & 1) << op->tb[j];
+            for (int j = 0; j < K; ++j) oc |= ((c >> j) & 1) << op.tb[j];
             const double2 x = tile[swz(base | oc)];
 #pragma unroll
             for (int j = 0; j < 4; ++j)
@@ -162,22 +260,22 @@ __device__ __noinline__ void dense_wide(double2* __restrict__ tile, const double
             if (j >= per) continue;
             const int r = lane + 32 * j;
             int orow = 0;
-            for (int b = 0; b < K; ++b) orow |= ((r >> b) & 1) << op->tb[b];
+            for (int b = 0; b < K; ++b) orow |= ((r >> b) & 1) << op.tb[b];
             tile[swz(base | orow)] = acc[j];
         }
         __syncwarp();
     }
 }
 
-__device__ __noinline__ void diagonal(double2* __restrict__ tile, const double2* __restrict__ d,
-                                      const GateOp* __restrict__ op, int E, std::uint64_t base) {
-    const int k = op->k;
+__device__ __forceinline__ void diagonal(double2* __restrict__ tile, const double2* __restrict__ d,
+                                         const GateOp& op, int E, std::uint64_t base) {
+    const int k = op.k;
     int fixed = 0, inmask = 0;
     int tb[kMaxDiagK];
 #pragma unroll
     for (int j = 0; j < kMaxDiagK; ++j) {
-        tb[j] = j < k ? op->tb[j] : -1;
-        if (j < k && tb[j] < 0) fixed |= static_cast<int>((base >> op->pos[j]) & 1ull) << j;
+        tb[j] = j < k ? op.tb[j] : -1;
+        if (j < k && tb[j] < 0) fixed |= static_cast<int>((base >> op.pos[j]) & 1ull) << j;
         if (tb[j] >= 0) inmask |= 1 << j;
     }
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
@@ -196,9 +294,10 @@ __device__ __noinline__ void diagonal(double2* __restrict__ tile, const double2*
 }
 
 __global__ void __launch_bounds__(kThreads, 2)
-    gate_pass_kernel(PePtrs ptrs, const PassHdr hdr, const GateOp* __restrict__ ops,
-                     const double2* __restrict__ pool) {
+    gate_pass_kernel(const __grid_constant__ PassParams P, const double2* __restrict__ pool,
+                     const double* __restrict__ frags) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    const PassHdr& hdr = P.hdr;
     const int T = hdr.T, E = 1 << T, c = hdr.c;
     double2* tile = reinterpret_cast<double2*>(smem_raw);
     double2* smat = tile + E;
@@ -218,24 +317,35 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int i = threadIdx.x; i < hdr.mat_count; i += blockDim.x) smat[i] = pool[hdr.mat_begin + i];
     __syncthreads();
 
-    amp_t* __restrict__ v = ptrs.p[blockIdx.y];
+    amp_t* __restrict__ v = P.ptrs.p[blockIdx.y];
     const int cmask = (1 << c) - 1;
-    for (int e = threadIdx.x; e < E; e += blockDim.x) tile[swz(e)] = __ldcs(&v[base | tab[e >> c] | (e & cmask)]);
+    for (int e = threadIdx.x; e < E; e += blockDim.x) cp_async16(&tile[swz(e)], &v[base | tab[e >> c] | (e & cmask)]);
+    cp_async_wait_all();
     __syncthreads();
 
     for (int o = 0; o < hdr.n_ops; ++o) {
-        const GateOp* op = ops + hdr.op_begin + o;
-        const int smo = op->smat;
-        const double2* u = smo >= 0 ? smat + smo : pool + op->gmat;
-        if (op->kind == kDiag) {
-            diagonal(tile, u, op, E, base);
+        const GateOp& op = P.ops[o];
+        const int kind = op.kind, k = op.k;
+        if (kind == kDiag) {
+            diagonal(tile, smat + op.smat, op, E, base);
         } else {
-            switch (op->k) {
-                case 1: dense_small<1>(tile, u, op, E); break;
-                case 2: dense_small<2>(tile, u, op, E); break;
-                case 3: dense_small<3>(tile, u, op, E); break;
-                case 4: dense_small<4>(tile, u, op, E); break;
-                default: dense_wide(tile, u, op, E); break;
+            const int pm = op.pmat;
+            switch (k) {
+                case 1: dense_small<1>(tile, P, pm, op, E); break;
+                case 2: dense_small<2>(tile, P, pm, op, E); break;
+                case 3:
+                    if (op.bfrag >= 0)
+                        dense_dmma<3>(tile, frags + op.bfrag, op, E);
+                    else
+                        dense_small<3>(tile, P, pm, op, E);
+                    break;
+                case 4:
+                    if (op.bfrag >= 0)
+                        dense_dmma<4>(tile, frags + op.bfrag, op, E);
+                    else
+                        dense_small<4>(tile, P, pm, op, E);
+                    break;
+                default: dense_wide(tile, pool + op.gmat, op, E); break;
             }
         }
         __syncthreads();
@@ -346,7 +456,7 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
         }
         Pass ps;
         std::uint64_t blocked = 0;
-        int mat_used = 0;
+        int param_used = 0, diag_used = 0;
         std::vector<int> keep;
         keep.reserve(remaining.size());
         bool closed = false;
@@ -369,10 +479,15 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
                 continue;
             }
             const bool fits = h.kind == kDiag || (h.mask & ~B) == 0;
-            const int staged = (h.kind == kDiag || h.k <= 4) ? h.mat_len : 0;
-            if (fits && mat_used + staged <= kMatBudget) {
+            const int T_here = whole ? nl : kTileBits;
+            const bool dmma = h.kind == kDense && (h.k == 3 || h.k == 4) && T_here >= h.k + 3;
+            const int in_params = (h.kind == kDense && h.k <= 4 && !dmma) ? h.mat_len : 0;
+            const int in_smem = h.kind == kDiag ? h.mat_len : 0;
+            if (fits && param_used + in_params <= kParamMats && diag_used + in_smem <= kDiagStage &&
+                static_cast<int>(ps.ops.size()) < kMaxPassOps) {
                 ps.ops.push_back(id);
-                mat_used += staged;
+                param_used += in_params;
+                diag_used += in_smem;
             } else {
                 blocked |= h.mask;
                 keep.push_back(id);
@@ -394,8 +509,11 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
     std::vector<GateOp> dev_ops;
     std::vector<PassHdr> hdrs;
     std::vector<double2> pool;
+    std::vector<std::vector<double2>> pmats(passes.size());
+    std::vector<double> frags;
     std::vector<int> wide_pos;  // for wide passes: positions (kBigK per pass)
-    for (Pass& ps : passes) {
+    for (std::size_t pidx = 0; pidx < passes.size(); ++pidx) {
+        Pass& ps = passes[pidx];
         PassHdr h{};
         if (ps.wide) {
             const HostOp& o = opsv[static_cast<std::size_t>(ps.ops[0])];
@@ -432,7 +550,13 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
         int tb_of[64];
         for (int p = 0; p < 64; ++p) tb_of[p] = -1;
         for (int i = 0; i < ps.T; ++i) tb_of[ps.tile_pos[static_cast<std::size_t>(i)]] = i;
-        // staged matrices first (contiguous), then global-only ones after
+        // diagonals staged contiguously in the pool (copied to smem per CTA),
+        // dense k<=4 matrices into the launch parameters, k=5..7 from global
+        auto put = [&](std::vector<double2>& dst, const HostOp& o) {
+            for (int e = 0; e < o.mat_len; ++e)
+                dst.push_back(make_double2(mats[o.mat_off + 2 * static_cast<std::size_t>(e)],
+                                           mats[o.mat_off + 2 * static_cast<std::size_t>(e) + 1]));
+        };
         int staged = 0;
         std::vector<std::pair<int, int>> late;  // (op index in dev_ops, host op)
         for (int id : ps.ops) {
@@ -440,30 +564,41 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
             GateOp g{};
             g.kind = o.kind;
             g.k = o.k;
+            g.smat = g.pmat = g.bfrag = -1;
             for (int j = 0; j < o.k; ++j) {
                 g.tb[j] = tb_of[o.pos[j]];
                 g.pos[j] = o.pos[j];
             }
-            if (o.kind == kDiag || o.k <= 4) {
+            if (o.kind == kDiag) {
                 g.smat = staged;
                 g.gmat = h.mat_begin + staged;
-                for (int e = 0; e < o.mat_len; ++e)
-                    pool.push_back(make_double2(mats[o.mat_off + 2 * static_cast<std::size_t>(e)],
-                                                mats[o.mat_off + 2 * static_cast<std::size_t>(e) + 1]));
+                put(pool, o);
                 staged += o.mat_len;
+            } else if ((o.k == 3 || o.k == 4) && ps.T >= o.k + 3) {
+                // DMMA B fragments of M^T, M = real form of U (see dense_dmma)
+                const int D = 1 << o.k, R = 2 * D, NB = R / 8, KB = R / 4;
+                g.bfrag = static_cast<int>(frags.size());
+                for (int nb = 0; nb < NB; ++nb)
+                    for (int kb = 0; kb < KB; ++kb)
+                        for (int lane = 0; lane < 32; ++lane) {
+                            const int kk = 4 * kb + (lane & 3), nn = 8 * nb + (lane >> 2);
+                            const int r = nn >> 1, i = nn & 1, c = kk >> 1, j = kk & 1;
+                            const std::size_t at = o.mat_off + 2 * (static_cast<std::size_t>(r) * D + c);
+                            const double re = mats[at], im = mats[at + 1];
+                            frags.push_back(i == j ? re : (i == 0 ? -im : im));
+                        }
+            } else if (o.k <= 4) {
+                g.pmat = static_cast<int>(pmats[pidx].size());
+                put(pmats[pidx], o);
             } else {
-                g.smat = -1;
                 late.emplace_back(static_cast<int>(dev_ops.size()), id);
             }
             dev_ops.push_back(g);
         }
         h.mat_count = staged;
         for (auto [di, id] : late) {
-            const HostOp& o = opsv[static_cast<std::size_t>(id)];
             dev_ops[static_cast<std::size_t>(di)].gmat = static_cast<int>(pool.size());
-            for (int e = 0; e < o.mat_len; ++e)
-                pool.push_back(make_double2(mats[o.mat_off + 2 * static_cast<std::size_t>(e)],
-                                            mats[o.mat_off + 2 * static_cast<std::size_t>(e) + 1]));
+            put(pool, opsv[static_cast<std::size_t>(id)]);
         }
         hdrs.push_back(h);
     }
@@ -472,17 +607,20 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
     const std::size_t pool_off = (ops_bytes + 255) & ~std::size_t{255};
     const std::size_t pool_bytes = pool.size() * sizeof(double2);
     const std::size_t wpos_off = (pool_off + pool_bytes + 255) & ~std::size_t{255};
-    const std::size_t total = wpos_off + wide_pos.size() * sizeof(int) + 16;
+    const std::size_t frag_off = (wpos_off + wide_pos.size() * sizeof(int) + 255) & ~std::size_t{255};
+    const std::size_t total = frag_off + frags.size() * sizeof(double) + 16;
     char* host = static_cast<char*>(ensure_pinned(st, total));
     QRT_CUDA(cudaStreamSynchronize(st->stream));  // pinned buffer may still feed a previous copy
     std::memcpy(host, dev_ops.data(), ops_bytes);
     std::memcpy(host + pool_off, pool.data(), pool_bytes);
     std::memcpy(host + wpos_off, wide_pos.data(), wide_pos.size() * sizeof(int));
+    std::memcpy(host + frag_off, frags.data(), frags.size() * sizeof(double));
     char* dev = static_cast<char*>(ensure_ops(st, total));
     QRT_CUDA(cudaMemcpyAsync(dev, host, total, cudaMemcpyHostToDevice, st->stream));
     const GateOp* d_ops = reinterpret_cast<const GateOp*>(dev);
     const double2* d_pool = reinterpret_cast<const double2*>(dev + pool_off);
     const int* d_wpos = reinterpret_cast<const int*>(dev + wpos_off);
+    const double* d_frags = reinterpret_cast<const double*>(dev + frag_off);
 
     static bool attr_done[64] = {};
     if (!attr_done[st->device]) {
@@ -490,7 +628,7 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
         attr_done[st->device] = true;
     }
 
-    PePtrs ptrs{};
+    static thread_local PassParams params;  // 29 KiB: keep off the stack
     ProfileScope prof(st, QRT_K_GATES);
     const double amps_all = static_cast<double>(st->amps) * st->pe_count;
     for (std::size_t pi = 0; pi < hdrs.size(); ++pi) {
@@ -512,13 +650,16 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
             st->stats[QRT_K_GATES].flops += 8.0 * (g.kind == kDiag ? 1.0 : static_cast<double>(1 << g.k)) * amps_all;
             continue;
         }
-        for (int i = 0; i < st->pe_count; ++i) ptrs.p[i] = st->live(i);
+        for (int i = 0; i < st->pe_count; ++i) params.ptrs.p[i] = st->live(i);
+        params.hdr = h;
+        std::copy(dev_ops.begin() + h.op_begin, dev_ops.begin() + h.op_begin + h.n_ops, params.ops);
+        std::copy(pmats[pi].begin(), pmats[pi].end(), params.mats);
         const int tiles = 1 << (st->nl - h.T);
         const std::size_t smem = (static_cast<std::size_t>(1) << h.T) * sizeof(double2) +
                                  static_cast<std::size_t>(h.mat_count) * sizeof(double2) +
                                  (static_cast<std::size_t>(1) << (h.T - h.c)) * sizeof(std::uint64_t);
         dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(st->pe_count));
-        gate_pass_kernel<<<grid, kThreads, smem, st->stream>>>(ptrs, h, d_ops, d_pool);
+        gate_pass_kernel<<<grid, kThreads, smem, st->stream>>>(params, d_pool, d_frags);
         QRT_CUDA(cudaGetLastError());
         st->stats[QRT_K_GATES].launches++;
         st->stats[QRT_K_GATES].bytes += 32.0 * amps_all;

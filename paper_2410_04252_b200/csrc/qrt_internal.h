@@ -32,7 +32,6 @@ inline constexpr int kMaxLocalPEs = 64;  // PEs one process may own
 inline constexpr int kTileBits = 12;     // smem tile: 2^12 amplitudes = 64 KiB
 inline constexpr int kCoalBits = 4;      // low positions always inside a tile (256 B runs)
 inline constexpr int kMaxTileGateK = 7;  // dense gates up to 7 qubits run inside a tile
-inline constexpr int kMatBudget = 2048;  // max double2 matrix entries staged per pass (32 KiB)
 inline constexpr int kThreads = 256;
 
 }  // namespace qrt

@@ -2,18 +2,24 @@
 // (reference local_pauli_expectation + expectation, dist_sim.cpp:84-97 and
 // :289-298) and the state norm (:115-120).
 //
-// Terms are batched by their X|Y flip mask.  For a flip mask x != 0 the pair
-// (i, i^x) contributes  s(i) [w + (-1)^{#Y} conj(w)],  w = conj(v[i^x]) v[i],
-// so only the canonical half of the pairs is visited and only Re(w) or Im(w)
-// is needed: the X/Y flip and the Z/Y phase are applied in registers.  Terms
-// with x = 0 (I/Z words) are evaluated from a Walsh-Hadamard transform of
-// |v|^2 over the tile, so their cost per CTA is O(1) per term.
+// Terms are batched by their X|Y flip mask x.  For x != 0 the pair (i, i^x)
+// contributes  s_t(i) [w + (-1)^{#Y} conj(w)],  w = conj(v[i^x]) v[i],
+// s_t(i) = (-1)^{popc(i & (z|y))}, so only the canonical half of the pairs is
+// visited and only Re(w) or Im(w) is needed: the X/Y flip and the Z/Y phase
+// are applied in registers.  Within a group the sign masks differ in only a
+// few bits D (for Jordan-Wigner words: the Y letters), so
+//   sum_t F_t s_t(i) val_t(i) = (-1)^{popc(i & m0)} (C_re[k] Re w + C_im[k] Im w),
+//   k = the bits of i at D,
+// with a 2^|D|-entry coefficient table built once per group per CTA: the
+// per-pair cost no longer grows with the number of terms.  Terms with x = 0
+// (I/Z words) are read off a Walsh-Hadamard transform of |v|^2 over the
+// tile, O(1) per term per CTA.
 //
-// A pass loads a 2^12-amplitude tile (positions B, chosen so the flip masks of
-// many groups lie inside B) into shared memory once and evaluates every group
-// it covers; per-CTA partial sums are reduced in a fixed order (warp shuffle
-// -> block -> deterministic tree per PE), so results are run-to-run
-// identical.  Algorithmic traffic per pass = 16 B x 2^(n-g) read.
+// A pass loads a 2^12-amplitude tile (positions B chosen so the flip masks of
+// many groups lie inside B) into shared memory once (cp.async) and evaluates
+// every group it covers.  Per-CTA partial sums are reduced in a fixed order
+// (warp shuffle -> block -> deterministic tree per PE), so results are
+// run-to-run identical.  Algorithmic traffic per pass = 16 B x 2^(n-g) read.
 
 #include <algorithm>
 #include <cstring>
@@ -25,23 +31,30 @@ namespace qrt {
 
 namespace {
 
+constexpr int kMaxDiffBits = 5;  // coefficient table of <= 32 entries per group
+
 struct PePtrsP {
     const amp_t* p[kMaxLocalPEs];
 };
 
 struct PTerm {
-    std::uint64_t m;   // sign mask (z|y) over local positions
+    std::uint64_t m;   // sign mask bits outside the tile (outer parity per CTA); full mask for I/Z words
     std::uint64_t gz;  // PE-index sign mask
     double2 f;         // folded coefficient (x2 and i^#Y for flip terms)
-    int m_tile;        // m restricted to the tile, in tile-bit indices
+    int dk;            // sign-mask difference to the group's m0, in table-index bits
     int comp;          // 0: Re(w), 1: Im(w)
+    int m_tile;        // I/Z words: sign mask in tile-bit indices
+    int pad;
 };
 
 struct PGroup {
-    int xy_tile;
-    int hbit;
-    int t_begin;
-    int t_count;
+    int xy_tile;  // flip mask in tile-bit indices
+    int hbit;     // canonical bit (top bit of xy_tile)
+    int t_begin, t_count;
+    int m0_tile;  // common sign mask (first term), tile-bit indices
+    int nd;       // |D|
+    int dpos[kMaxDiffBits];
+    int need;     // bit 0: some term reads Re(w), bit 1: some term reads Im(w)
 };
 
 struct PPass {
@@ -53,14 +66,15 @@ struct PPass {
     int pe_begin;
 };
 
-__device__ __forceinline__ int swz(int e) {
-    int x = e >> 3;
-    return e ^ ((x ^ (x >> 3) ^ (x >> 6) ^ (x >> 9)) & 7);
-}
 __device__ __forceinline__ int insert_zero(int v, int bit) {
     return ((v >> bit) << (bit + 1)) | (v & ((1 << bit) - 1));
 }
 __device__ __forceinline__ double flip_if(double v, int odd) { return odd ? -v : v; }
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
 
 __device__ __forceinline__ double2 block_sum(double2 v, double2* scratch) {
 #pragma unroll
@@ -81,11 +95,45 @@ __device__ __forceinline__ double2 block_sum(double2 v, double2* scratch) {
     return r;
 }
 
+// The pair loop of one group; NEED selects Re(w) / Im(w) / both at compile time.
+template <int NEED>
+__device__ __forceinline__ double2 group_pairs(const double2* __restrict__ tile, const PGroup& G,
+                                               const double4* __restrict__ tbl, int half, int lane) {
+    double2 acc = make_double2(0.0, 0.0);
+    const int X = G.xy_tile, h = G.hbit, m0 = G.m0_tile, nd = G.nd;
+    int dpos[kMaxDiffBits];
+#pragma unroll
+    for (int i = 0; i < kMaxDiffBits; ++i) dpos[i] = G.dpos[i];
+    for (int idx = lane; idx < half; idx += 32) {
+        const int e = insert_zero(idx, h);
+        const double2 a = tile[e ^ X];
+        const double2 b = tile[e];
+        int k = 0;
+#pragma unroll
+        for (int i = 0; i < kMaxDiffBits; ++i)
+            if (i < nd) k |= ((e >> dpos[i]) & 1) << i;
+        const double4 cf = tbl[k];  // (C_re.x, C_re.y, C_im.x, C_im.y)
+        const int odd = __popc(e & m0) & 1;
+        if (NEED & 1) {
+            const double re = flip_if(fma(a.x, b.x, a.y * b.y), odd);
+            acc.x = fma(cf.x, re, acc.x);
+            acc.y = fma(cf.y, re, acc.y);
+        }
+        if (NEED & 2) {
+            const double im = flip_if(fma(a.x, b.y, -a.y * b.x), odd);
+            acc.x = fma(cf.z, im, acc.x);
+            acc.y = fma(cf.w, im, acc.y);
+        }
+    }
+    return acc;
+}
+
 __global__ void __launch_bounds__(kThreads, 2)
     pauli_pass_kernel(PePtrsP ptrs, const PPass P, const PGroup* __restrict__ groups, const PTerm* __restrict__ terms,
                       double* __restrict__ red) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double2 scratch[kThreads / 32];
+    __shared__ double4 tables[kThreads / 32][1 << kMaxDiffBits];
     const int T = P.T, E = 1 << T, c = P.c;
     double2* tile = reinterpret_cast<double2*>(smem_raw);
     std::uint64_t* tab = reinterpret_cast<std::uint64_t*>(tile + E);
@@ -102,15 +150,17 @@ __global__ void __launch_bounds__(kThreads, 2)
     const amp_t* __restrict__ v = ptrs.p[blockIdx.y];
     const std::uint64_t pe = static_cast<std::uint64_t>(P.pe_begin) + blockIdx.y;
     const int cmask = (1 << c) - 1;
-    for (int e = threadIdx.x; e < E; e += blockDim.x) {
-        const double2 a = __ldcs(&v[base | tab[e >> c] | (e & cmask)]);
-        tile[swz(e)] = a;
-        if (P.d_count > 0) W[e] = fma(a.x, a.x, a.y * a.y);
-    }
+    for (int e = threadIdx.x; e < E; e += blockDim.x) cp_async16(&tile[e], &v[base | tab[e >> c] | (e & cmask)]);
+    asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
 
     double2 acc = make_double2(0.0, 0.0);
-    if (P.d_count > 0) {  // diagonal words: WHT of |v|^2 over the tile
+    if (P.d_count > 0) {  // I/Z words: WHT of |v|^2 over the tile
+        for (int e = threadIdx.x; e < E; e += blockDim.x) {
+            const double2 a = tile[e];
+            W[e] = fma(a.x, a.x, a.y * a.y);
+        }
+        __syncthreads();
         for (int s = 0; s < T; ++s) {
             for (int i = threadIdx.x; i < (E >> 1); i += blockDim.x) {
                 const int i0 = insert_zero(i, s), i1 = i0 | (1 << s);
@@ -131,42 +181,36 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int half = E >> 1;
+    double4* tbl = tables[warp];
     for (int gi = warp; gi < P.g_count; gi += nwarps) {
         const PGroup G = groups[P.g_begin + gi];
-        for (int t0 = 0; t0 < G.t_count; t0 += 4) {
-            const int nt = min(4, G.t_count - t0);
-            double2 F[4];
-            int mt[4], cp[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (q < nt) {
-                    const PTerm tm = terms[G.t_begin + t0 + q];
-                    const int odd = (__popcll(base & tm.m) + __popcll(pe & tm.gz)) & 1;
-                    F[q] = make_double2(flip_if(tm.f.x, odd), flip_if(tm.f.y, odd));
-                    mt[q] = tm.m_tile;
-                    cp[q] = tm.comp;
+        // coefficient table: entry k = sum_t F_t (-1)^{outer_t + pe_t + popc(k & dk_t)}
+        if (lane < (1 << G.nd)) {
+            double4 e4 = make_double4(0.0, 0.0, 0.0, 0.0);
+            for (int t = 0; t < G.t_count; ++t) {
+                const PTerm tm = terms[G.t_begin + t];
+                const int odd = (__popcll(base & tm.m) + __popcll(pe & tm.gz) + __popc(lane & tm.dk)) & 1;
+                const double fx = flip_if(tm.f.x, odd), fy = flip_if(tm.f.y, odd);
+                if (tm.comp) {
+                    e4.z += fx;
+                    e4.w += fy;
                 } else {
-                    F[q] = make_double2(0.0, 0.0);
-                    mt[q] = 0;
-                    cp[q] = 0;
+                    e4.x += fx;
+                    e4.y += fy;
                 }
             }
-            for (int idx = lane; idx < half; idx += 32) {
-                const int e = insert_zero(idx, G.hbit);
-                const double2 a = tile[swz(e ^ G.xy_tile)];
-                const double2 b = tile[swz(e)];
-                const double re = fma(a.x, b.x, a.y * b.y);
-                const double im = fma(a.x, b.y, -a.y * b.x);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    if (q < nt) {
-                        const double val = flip_if(cp[q] ? im : re, __popc(e & mt[q]) & 1);
-                        acc.x = fma(F[q].x, val, acc.x);
-                        acc.y = fma(F[q].y, val, acc.y);
-                    }
-                }
-            }
+            tbl[lane] = e4;
         }
+        __syncwarp();
+        double2 g;
+        switch (G.need) {
+            case 1: g = group_pairs<1>(tile, G, tbl, half, lane); break;
+            case 2: g = group_pairs<2>(tile, G, tbl, half, lane); break;
+            default: g = group_pairs<3>(tile, G, tbl, half, lane); break;
+        }
+        acc.x += g.x;
+        acc.y += g.y;
+        __syncwarp();
     }
     const double2 tot = block_sum(acc, scratch);
     if (threadIdx.x == 0) {
@@ -228,6 +272,12 @@ void gather_partials(qrt_state* st, const double* d_local, double* all) {
     }
 }
 
+int compress_bits(std::uint64_t m, const int* tile_pos, int T) {
+    int r = 0;
+    for (int i = 0; i < T; ++i) r |= static_cast<int>((m >> tile_pos[i]) & 1ull) << i;
+    return r;
+}
+
 }  // namespace
 
 void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const std::uint64_t* y,
@@ -243,7 +293,7 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
     for (int i = 0; i < 2 * st->p; ++i) partial[i] = 0.0;
     if (n_terms == 0) return;
 
-    // ---- group by flip mask ------------------------------------------------
+    // ---- group by flip mask -------------------------------------------------
     std::map<std::uint64_t, std::vector<int>> by_xy;
     for (int t = 0; t < n_terms; ++t) by_xy[x[t] | y[t]].push_back(t);
     std::vector<int> diag;
@@ -255,7 +305,7 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
             flips.emplace_back(kv.first, kv.second);
     }
 
-    // ---- passes: choose tile positions covering many flip masks -------------
+    // ---- passes: tile positions covering many flip masks --------------------
     const int T = std::min(kTileBits, nl);
     const int coal = std::min(kCoalBits, nl);
     struct Pass {
@@ -266,13 +316,12 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
     std::vector<Pass> passes;
     std::vector<int> left(flips.size());
     for (std::size_t i = 0; i < flips.size(); ++i) left[i] = static_cast<int>(i);
-    // widest masks first so they seed the tiles
     std::stable_sort(left.begin(), left.end(), [&](int a, int b) {
         return popc(flips[static_cast<std::size_t>(a)].first) > popc(flips[static_cast<std::size_t>(b)].first);
     });
     bool diag_done = diag.empty();
     while (!left.empty() || !diag_done) {
-        std::uint64_t B = (coal >= 64) ? ~0ull : ((1ull << coal) - 1);
+        std::uint64_t B = (1ull << coal) - 1;
         if (T == nl) {
             B = local_mask;
         } else {
@@ -293,15 +342,10 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
         left.swap(keep);
     }
 
-    // ---- device descriptors --------------------------------------------------
+    // ---- device descriptors ---------------------------------------------------
     std::vector<PGroup> dgroups;
     std::vector<PTerm> dterms;
     std::vector<PPass> hdrs;
-    auto compress = [](std::uint64_t m, const int* tile_pos, int Tn) {
-        int r = 0;
-        for (int i = 0; i < Tn; ++i) r |= static_cast<int>((m >> tile_pos[i]) & 1ull) << i;
-        return r;
-    };
     for (const Pass& ps : passes) {
         PPass h{};
         h.T = T;
@@ -324,34 +368,59 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
                 tm.m = z[t] | y[t];
                 tm.gz = gz[t];
                 tm.f = make_double2(coeffs[2 * t], coeffs[2 * t + 1]);
-                tm.m_tile = compress(tm.m & ps.B, h.tile_pos, T);
-                tm.comp = 0;
+                tm.m_tile = compress_bits(tm.m & ps.B, h.tile_pos, T);
                 dterms.push_back(tm);
             }
             h.d_count = static_cast<int>(diag.size());
         }
         h.g_begin = static_cast<int>(dgroups.size());
-        h.g_count = static_cast<int>(ps.groups.size());
         for (int gi : ps.groups) {
             const auto& [xy, members] = flips[static_cast<std::size_t>(gi)];
-            PGroup G{};
-            G.xy_tile = compress(xy, h.tile_pos, T);
-            G.hbit = 31 - __builtin_clz(static_cast<unsigned>(G.xy_tile));
-            G.t_begin = static_cast<int>(dterms.size());
-            G.t_count = static_cast<int>(members.size());
-            for (int t : members) {
-                const int ycnt = popc(y[t]);
-                const double sgn = ((ycnt & 3) == 1 || (ycnt & 3) == 2) ? -2.0 : 2.0;
-                PTerm tm{};
-                tm.m = z[t] | y[t];
-                tm.gz = gz[t];
-                tm.f = make_double2(sgn * coeffs[2 * t], sgn * coeffs[2 * t + 1]);
-                tm.m_tile = compress(tm.m & ps.B, h.tile_pos, T);
-                tm.comp = ycnt & 1;
-                dterms.push_back(tm);
+            // chunks whose sign masks differ from the first in <= kMaxDiffBits tile bits
+            std::size_t at = 0;
+            while (at < members.size()) {
+                const int t0 = members[at];
+                const int m0 = compress_bits((z[t0] | y[t0]) & ps.B, h.tile_pos, T);
+                int D = 0;
+                std::size_t end = at;
+                while (end < members.size()) {
+                    const int t = members[end];
+                    const int d = compress_bits((z[t] | y[t]) & ps.B, h.tile_pos, T) ^ m0;
+                    if (popc(static_cast<std::uint64_t>(D | d)) > kMaxDiffBits) break;
+                    D |= d;
+                    ++end;
+                }
+                PGroup G{};
+                G.xy_tile = compress_bits(xy, h.tile_pos, T);
+                G.hbit = 31 - __builtin_clz(static_cast<unsigned>(G.xy_tile));
+                G.m0_tile = m0;
+                G.nd = 0;
+                for (int b = 0; b < T; ++b)
+                    if (D >> b & 1) G.dpos[G.nd++] = b;
+                G.t_begin = static_cast<int>(dterms.size());
+                G.t_count = static_cast<int>(end - at);
+                G.need = 0;
+                for (std::size_t q = at; q < end; ++q) {
+                    const int t = members[q];
+                    const int ycnt = popc(y[t]);
+                    const double sgn = ((ycnt & 3) == 1 || (ycnt & 3) == 2) ? -2.0 : 2.0;
+                    PTerm tm{};
+                    tm.m = (z[t] | y[t]) & ~ps.B;  // outer parity: bits outside the tile only
+                    tm.gz = gz[t];
+                    tm.f = make_double2(sgn * coeffs[2 * t], sgn * coeffs[2 * t + 1]);
+                    const int d = compress_bits((z[t] | y[t]) & ps.B, h.tile_pos, T) ^ m0;
+                    int dk = 0;
+                    for (int i = 0; i < G.nd; ++i) dk |= ((d >> G.dpos[i]) & 1) << i;
+                    tm.dk = dk;
+                    tm.comp = ycnt & 1;
+                    G.need |= tm.comp ? 2 : 1;
+                    dterms.push_back(tm);
+                }
+                dgroups.push_back(G);
+                at = end;
             }
-            dgroups.push_back(G);
         }
+        h.g_count = static_cast<int>(dgroups.size()) - h.g_begin;
         hdrs.push_back(h);
     }
     const std::size_t gbytes = dgroups.size() * sizeof(PGroup);

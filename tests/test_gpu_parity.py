@@ -293,11 +293,11 @@ def test_large_qr_roundtrip_and_norm(qb, device):
     ids = [op.id for op in c.operators if all(q < n - 2 for q in op.targets)]
     qb.apply_gates_narrow(st, c, ids)
     before = [st.sub_of(pe) for pe in range(p)]
-    lay0 = st.layout
+    locals0 = st.layout.local_set()  # st.layout is a live view; keep the value
     ev = qb.make_qr_event(st.layout, ((1 << n) - 1) & ~0b11)  # qubits 0,1 <-> 24,25
     qb.perform_qr(st, ev)
     assert st.last_relocated == qb.qr_data_volume(2, n)
-    back = qb.make_qr_event(st.layout, lay0.local_set())
+    back = qb.make_qr_event(st.layout, locals0)
     qb.perform_qr(st, back)
     for pe in range(p):
         assert np.array_equal(st.sub_of(pe), before[pe])

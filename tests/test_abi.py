@@ -1,0 +1,63 @@
+"""The C-ABI library (CPU only: no compute calls without a GPU).
+
+libqrt.so must load, export every entry point declared in include/qrt.h, and
+fail loudly (QRT_ERR_NO_DEVICE + a message) when no device is present — the
+product has no CPU fallback.
+"""
+import ctypes as C
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = (ROOT / "include" / "qrt.h").read_text()
+
+
+def declared():
+    names = re.findall(r"^\s*(?:qrt_status|const char\*|int)\s+(qrt_\w+)\s*\(", HEADER, flags=re.M)
+    assert len(names) >= 15
+    return names
+
+
+def test_exports_every_declared_symbol(qb):
+    lib = qb.load_libqrt()
+    missing = [n for n in declared() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_abi_version_and_codes(qb):
+    lib = qb.load_libqrt()
+    assert lib.qrt_abi_version() == qb.QRT_ABI_VERSION == 1
+    lib.qrt_last_error.restype = C.c_char_p
+    assert isinstance(lib.qrt_last_error(), bytes)
+
+
+def test_no_device_fails_loudly(qb):
+    lib = qb.load_libqrt()
+    n = C.c_int(-1)
+    assert lib.qrt_device_count(C.byref(n)) == 0
+    if n.value > 0:
+        pytest.skip("a GPU is visible; covered by the gpu suite")
+    st = C.c_void_p()
+    rc = lib.qrt_state_create(4, 1, 0, None, C.byref(st))
+    assert rc == 11  # QRT_ERR_NO_DEVICE
+    lib.qrt_last_error.restype = C.c_char_p
+    assert b"device" in lib.qrt_last_error()
+    with pytest.raises(qb.DeviceError):
+        qb.init_state(4, qb.ClusterShape.flat(1))
+
+
+def test_argument_validation_without_device(qb):
+    lib = qb.load_libqrt()
+    st = C.c_void_p()
+    assert lib.qrt_state_create(4, 3, 0, None, C.byref(st)) == 7  # QRT_ERR_CONFIG: p not a power of two
+    assert lib.qrt_state_create(2, 8, 0, None, C.byref(st)) == 6  # QRT_ERR_TOO_MANY_PES
+    assert lib.qrt_state_destroy(None) == 0
+
+
+def test_native_libraries_are_in_tree(qb):
+    pkg = Path(qb.__file__).parent
+    for name in ("libqrt.so", "libqrtile_b200.so"):
+        assert (pkg / name).exists()
+    assert Path(qb._qrtile.__file__).parent == pkg

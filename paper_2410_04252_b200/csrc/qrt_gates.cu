@@ -17,6 +17,7 @@
 // flops per dense k-qubit gate = 8 x 2^k x 2^(n-g).
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "qrt_internal.h"
@@ -51,6 +52,8 @@ struct PassHdr {
     int op_begin;
     int mat_begin;       // first double2 of this pass's staged matrices in the pool
     int mat_count;
+    int frag_begin;      // first double of this pass's DMMA B fragments in the fragment pool
+    int frag_count;
     int n_outer;
     int tile_pos[kTileBits];
     int outer_pos[64];
@@ -63,6 +66,7 @@ struct PassHdr {
 constexpr int kParamMats = 1664;  // double2 entries, 26 KiB (all params <= 32 KiB)
 constexpr int kMaxPassOps = 40;   // op descriptors per pass, also in the parameters
 constexpr int kDiagStage = 1024; // diagonal entries staged in smem per pass
+constexpr int kFragStage = 6144; // DMMA B-fragment doubles staged in smem per pass (48 KiB)
 
 struct PassParams {
     PePtrs ptrs;
@@ -171,11 +175,6 @@ __device__ __forceinline__ void dense_dmma(double2* __restrict__ tile, const dou
                                            const GateOp& op, int E) {
     constexpr int D = 1 << K, R = 2 * D, NB = R / 8, KB = R / 4;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    double b[NB][KB];
-#pragma unroll
-    for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-        for (int kb = 0; kb < KB; ++kb) b[nb][kb] = __ldg(&frag[(nb * KB + kb) * 32 + lane]);
     int tb[K], sb[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) sb[j] = tb[j] = op.tb[j];
@@ -194,33 +193,51 @@ __device__ __forceinline__ void dense_dmma(double2* __restrict__ tile, const dou
         for (int j = 0; j < K; ++j) o |= ((m >> j) & 1) << tb[j];
         return o;
     };
-    // per-lane constant offsets: A columns (complex index 2kb + ((lane&3)>>1))
-    // and C rows (complex index 4nb + (lane&3))
-    int aoff[KB], coff[NB];
+    // swz is linear over GF(2), so swz(base | off) = swz(base) ^ swz(off)
+    // for disjoint bit sets: precompute the swizzled per-lane offsets once.
+    int sa[KB], sc[NB];
 #pragma unroll
-    for (int kb = 0; kb < KB; ++kb) aoff[kb] = spread(2 * kb + ((lane & 3) >> 1));
+    for (int kb = 0; kb < KB; ++kb) sa[kb] = swz(spread(2 * kb + ((lane & 3) >> 1)));
 #pragma unroll
-    for (int nb = 0; nb < NB; ++nb) coff[nb] = spread(4 * nb + (lane & 3));
+    for (int nb = 0; nb < NB; ++nb) sc[nb] = swz(spread(4 * nb + (lane & 3)));
     const int comp = lane & 1;
     double* __restrict__ tiled = reinterpret_cast<double*>(tile);
+    const double* __restrict__ fl = frag + lane;
     const int blocks = (E >> K) >> 3;
-    for (int rb = warp; rb < blocks; rb += nwarps) {
+    auto row_base = [&](int rb) {
         int base = rb * 8 + (lane >> 2);
 #pragma unroll
         for (int j = 0; j < K; ++j) base = insert_zero(base, sb[j]);
-        double a[KB];
+        return swz(base);
+    };
+    // two row-blocks per iteration: 2*NB independent accumulator chains
+    for (int rb = warp; rb < blocks; rb += 2 * nwarps) {
+        const int rb1 = rb + nwarps;
+        const bool two = rb1 < blocks;
+        const int s0 = row_base(rb), s1 = two ? row_base(rb1) : s0;
+        double a0[KB], a1[KB];
 #pragma unroll
-        for (int kb = 0; kb < KB; ++kb) a[kb] = tiled[2 * swz(base | aoff[kb]) + comp];
-        double acc[NB][2];
+        for (int kb = 0; kb < KB; ++kb) {
+            a0[kb] = tiled[2 * (s0 ^ sa[kb]) + comp];
+            a1[kb] = tiled[2 * (s1 ^ sa[kb]) + comp];
+        }
+        double c0[NB][2], c1[NB][2];
 #pragma unroll
-        for (int nb = 0; nb < NB; ++nb) acc[nb][0] = acc[nb][1] = 0.0;
-        // k-blocks outer: the NB accumulator chains interleave
+        for (int nb = 0; nb < NB; ++nb) c0[nb][0] = c0[nb][1] = c1[nb][0] = c1[nb][1] = 0.0;
 #pragma unroll
         for (int kb = 0; kb < KB; ++kb)
 #pragma unroll
-            for (int nb = 0; nb < NB; ++nb) dmma_8x8x4(acc[nb][0], acc[nb][1], a[kb], b[nb][kb]);
+            for (int nb = 0; nb < NB; ++nb) {
+                const double b = fl[(nb * KB + kb) * 32];
+                dmma_8x8x4(c0[nb][0], c0[nb][1], a0[kb], b);
+                dmma_8x8x4(c1[nb][0], c1[nb][1], a1[kb], b);
+            }
 #pragma unroll
-        for (int nb = 0; nb < NB; ++nb) tile[swz(base | coff[nb])] = make_double2(acc[nb][0], acc[nb][1]);
+        for (int nb = 0; nb < NB; ++nb) tile[s0 ^ sc[nb]] = make_double2(c0[nb][0], c0[nb][1]);
+        if (two) {
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) tile[s1 ^ sc[nb]] = make_double2(c1[nb][0], c1[nb][1]);
+        }
     }
 }
 
@@ -293,9 +310,12 @@ __device__ __forceinline__ void diagonal(double2* __restrict__ tile, const doubl
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 2)
+// One CTA per tile; several CTAs per SM so one CTA's load / store phase
+// overlaps another's fp64 math.  The pass's DMMA B fragments are read
+// through L1 (they are shared by every CTA of the pass).
+__global__ void __launch_bounds__(256, 2)
     gate_pass_kernel(const __grid_constant__ PassParams P, const double2* __restrict__ pool,
-                     const double* __restrict__ frags) {
+                     const double* __restrict__ frags, int tiles_per_pe) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const PassHdr& hdr = P.hdr;
     const int T = hdr.T, E = 1 << T, c = hdr.c;
@@ -303,10 +323,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     double2* smat = tile + E;
     std::uint64_t* tab = reinterpret_cast<std::uint64_t*>(smat + hdr.mat_count);
     const int nt = 1 << (T - c);
-
+    const int t = blockIdx.x;
     std::uint64_t base = 0;
     {
-        const std::uint64_t b = blockIdx.x;
+        const std::uint64_t b = static_cast<std::uint64_t>(t % tiles_per_pe);
         for (int i = 0; i < hdr.n_outer; ++i) base |= ((b >> i) & 1ull) << hdr.outer_pos[i];
     }
     for (int h = threadIdx.x; h < nt; h += blockDim.x) {
@@ -317,12 +337,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int i = threadIdx.x; i < hdr.mat_count; i += blockDim.x) smat[i] = pool[hdr.mat_begin + i];
     __syncthreads();
 
-    amp_t* __restrict__ v = P.ptrs.p[blockIdx.y];
+    amp_t* __restrict__ v = P.ptrs.p[t / tiles_per_pe];
     const int cmask = (1 << c) - 1;
     for (int e = threadIdx.x; e < E; e += blockDim.x) cp_async16(&tile[swz(e)], &v[base | tab[e >> c] | (e & cmask)]);
     cp_async_wait_all();
     __syncthreads();
 
+    const double* __restrict__ pf = frags + hdr.frag_begin;
     for (int o = 0; o < hdr.n_ops; ++o) {
         const GateOp& op = P.ops[o];
         const int kind = op.kind, k = op.k;
@@ -335,13 +356,13 @@ __global__ void __launch_bounds__(kThreads, 2)
                 case 2: dense_small<2>(tile, P, pm, op, E); break;
                 case 3:
                     if (op.bfrag >= 0)
-                        dense_dmma<3>(tile, frags + op.bfrag, op, E);
+                        dense_dmma<3>(tile, pf + op.bfrag, op, E);
                     else
                         dense_small<3>(tile, P, pm, op, E);
                     break;
                 case 4:
                     if (op.bfrag >= 0)
-                        dense_dmma<4>(tile, frags + op.bfrag, op, E);
+                        dense_dmma<4>(tile, pf + op.bfrag, op, E);
                     else
                         dense_small<4>(tile, P, pm, op, E);
                     break;
@@ -350,7 +371,6 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         __syncthreads();
     }
-
     for (int e = threadIdx.x; e < E; e += blockDim.x) __stcs(&v[base | tab[e >> c] | (e & cmask)], tile[swz(e)]);
 }
 
@@ -381,6 +401,27 @@ __global__ void wide_gate_kernel(const amp_t* __restrict__ in, amp_t* __restrict
         }
         out[i] = acc;
     }
+}
+
+// CTA size of the gate pass kernel: 128 (3 CTAs / SM) or 256 (2 CTAs / SM);
+// QRT_GATE_THREADS overrides for experiments.
+int gate_threads() {
+    static int v = [] {
+        const char* e = std::getenv("QRT_GATE_THREADS");
+        const int t = e ? std::atoi(e) : 128;
+        return (t == 256 || t == 128 || t == 64) ? t : 128;
+    }();
+    return v;
+}
+
+int sm_count(qrt_state* st) {
+    static int cached[64] = {};
+    if (!cached[st->device]) {
+        int v = 0;
+        QRT_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, st->device));
+        cached[st->device] = v;
+    }
+    return cached[st->device];
 }
 
 struct HostOp {
@@ -456,7 +497,7 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
         }
         Pass ps;
         std::uint64_t blocked = 0;
-        int param_used = 0, diag_used = 0;
+        int param_used = 0, diag_used = 0, frag_used = 0;
         std::vector<int> keep;
         keep.reserve(remaining.size());
         bool closed = false;
@@ -483,11 +524,13 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
             const bool dmma = h.kind == kDense && (h.k == 3 || h.k == 4) && T_here >= h.k + 3;
             const int in_params = (h.kind == kDense && h.k <= 4 && !dmma) ? h.mat_len : 0;
             const int in_smem = h.kind == kDiag ? h.mat_len : 0;
+            const int in_frag = dmma ? 4 * h.mat_len : 0;  // (2D)^2 real entries
             if (fits && param_used + in_params <= kParamMats && diag_used + in_smem <= kDiagStage &&
-                static_cast<int>(ps.ops.size()) < kMaxPassOps) {
+                frag_used + in_frag <= kFragStage && static_cast<int>(ps.ops.size()) < kMaxPassOps) {
                 ps.ops.push_back(id);
                 param_used += in_params;
                 diag_used += in_smem;
+                frag_used += in_frag;
             } else {
                 blocked |= h.mask;
                 keep.push_back(id);
@@ -558,6 +601,7 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
                                            mats[o.mat_off + 2 * static_cast<std::size_t>(e) + 1]));
         };
         int staged = 0;
+        h.frag_begin = static_cast<int>(frags.size());
         std::vector<std::pair<int, int>> late;  // (op index in dev_ops, host op)
         for (int id : ps.ops) {
             const HostOp& o = opsv[static_cast<std::size_t>(id)];
@@ -577,7 +621,7 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
             } else if ((o.k == 3 || o.k == 4) && ps.T >= o.k + 3) {
                 // DMMA B fragments of M^T, M = real form of U (see dense_dmma)
                 const int D = 1 << o.k, R = 2 * D, NB = R / 8, KB = R / 4;
-                g.bfrag = static_cast<int>(frags.size());
+                g.bfrag = static_cast<int>(frags.size()) - h.frag_begin;
                 for (int nb = 0; nb < NB; ++nb)
                     for (int kb = 0; kb < KB; ++kb)
                         for (int lane = 0; lane < 32; ++lane) {
@@ -596,6 +640,7 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
             dev_ops.push_back(g);
         }
         h.mat_count = staged;
+        h.frag_count = static_cast<int>(frags.size()) - h.frag_begin;
         for (auto [di, id] : late) {
             dev_ops[static_cast<std::size_t>(di)].gmat = static_cast<int>(pool.size());
             put(pool, opsv[static_cast<std::size_t>(id)]);
@@ -655,11 +700,11 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
         std::copy(dev_ops.begin() + h.op_begin, dev_ops.begin() + h.op_begin + h.n_ops, params.ops);
         std::copy(pmats[pi].begin(), pmats[pi].end(), params.mats);
         const int tiles = 1 << (st->nl - h.T);
+        const int total_tiles = tiles * st->pe_count;
         const std::size_t smem = (static_cast<std::size_t>(1) << h.T) * sizeof(double2) +
                                  static_cast<std::size_t>(h.mat_count) * sizeof(double2) +
                                  (static_cast<std::size_t>(1) << (h.T - h.c)) * sizeof(std::uint64_t);
-        dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(st->pe_count));
-        gate_pass_kernel<<<grid, kThreads, smem, st->stream>>>(params, d_pool, d_frags);
+        gate_pass_kernel<<<total_tiles, gate_threads(), smem, st->stream>>>(params, d_pool, d_frags, tiles);
         QRT_CUDA(cudaGetLastError());
         st->stats[QRT_K_GATES].launches++;
         st->stats[QRT_K_GATES].bytes += 32.0 * amps_all;

@@ -473,49 +473,28 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
         return h.kind == kDiag ? h.k > kMaxDiagK : h.k > kMaxTileGateK;
     };
     const bool whole = nl <= kTileBits;
-    while (!remaining.empty()) {
-        std::uint64_t B = 0;
-        if (whole) {
-            B = (nl >= 64) ? ~0ull : ((1ull << nl) - 1);
-        } else {
-            B = (1ull << kCoalBits) - 1;
-            std::uint64_t blocked = 0;
-            for (int id : remaining) {
-                const HostOp& h = opsv[static_cast<std::size_t>(id)];
-                if (h.kind == kDiag) {
-                    if (h.mask & blocked) blocked |= h.mask;
-                    continue;
-                }
-                if ((h.mask & blocked) || is_wide(h) || __builtin_popcountll(B | h.mask) > kTileBits) {
-                    blocked |= h.mask;
-                    continue;
-                }
-                B |= h.mask;
-                if (__builtin_popcountll(B) == kTileBits) break;
-            }
-            for (int p = 0; p < nl && __builtin_popcountll(B) < kTileBits; ++p) B |= 1ull << p;
-        }
-        Pass ps;
+    // The take phase for tile positions B: in order, every gate whose targets
+    // are inside B (diagonals anywhere) unless it follows a deferred gate on a
+    // shared qubit or the per-pass staging budgets are exhausted.
+    auto take = [&](std::uint64_t B, Pass* ps, std::vector<int>* keep) -> int {
         std::uint64_t blocked = 0;
-        int param_used = 0, diag_used = 0, frag_used = 0;
-        std::vector<int> keep;
-        keep.reserve(remaining.size());
-        bool closed = false;
+        int param_used = 0, diag_used = 0, frag_used = 0, n = 0;
+        bool closed = false, wide = false;
         for (int id : remaining) {
             const HostOp& h = opsv[static_cast<std::size_t>(id)];
             if (closed || (h.mask & blocked)) {
                 blocked |= h.mask;
-                keep.push_back(id);
+                if (keep) keep->push_back(id);
                 continue;
             }
             if (is_wide(h)) {
-                if (ps.ops.empty()) {  // runs alone, out of place
-                    ps.wide = true;
-                    ps.ops.push_back(id);
-                    closed = true;
+                if (n == 0) {  // runs alone, out of place
+                    wide = closed = true;
+                    ++n;
+                    if (ps) ps->ops.push_back(id);
                 } else {
                     blocked |= h.mask;
-                    keep.push_back(id);
+                    if (keep) keep->push_back(id);
                 }
                 continue;
             }
@@ -526,16 +505,66 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
             const int in_smem = h.kind == kDiag ? h.mat_len : 0;
             const int in_frag = dmma ? 4 * h.mat_len : 0;  // (2D)^2 real entries
             if (fits && param_used + in_params <= kParamMats && diag_used + in_smem <= kDiagStage &&
-                frag_used + in_frag <= kFragStage && static_cast<int>(ps.ops.size()) < kMaxPassOps) {
-                ps.ops.push_back(id);
+                frag_used + in_frag <= kFragStage && n < kMaxPassOps) {
+                ++n;
+                if (ps) ps->ops.push_back(id);
                 param_used += in_params;
                 diag_used += in_smem;
                 frag_used += in_frag;
             } else {
                 blocked |= h.mask;
-                keep.push_back(id);
+                if (keep) keep->push_back(id);
             }
         }
+        if (ps) ps->wide = wide;
+        return n;
+    };
+    // Candidate tile positions seeded from one of the first remaining gates:
+    // grow B from the coalescing bits by the targets of gates in order
+    // (rotated to start at the seed), skipping gates that are blocked or
+    // would overflow the tile.  The candidate that takes most gates wins
+    // (ties: the earliest seed).  Seeding from several gates lets a pass
+    // follow the light cone of the circuit instead of the first layer only.
+    constexpr int kSeeds = 16;
+    auto candidate = [&](std::size_t seed) {
+        std::uint64_t B = (1ull << kCoalBits) - 1, blocked = 0;
+        const std::size_t m = remaining.size();
+        for (std::size_t q = 0; q < m; ++q) {
+            const HostOp& h = opsv[static_cast<std::size_t>(remaining[(seed + q) % m])];
+            if (h.kind == kDiag) {
+                if (h.mask & blocked) blocked |= h.mask;
+                continue;
+            }
+            if ((h.mask & blocked) || is_wide(h) || __builtin_popcountll(B | h.mask) > kTileBits) {
+                blocked |= h.mask;
+                continue;
+            }
+            B |= h.mask;
+            if (__builtin_popcountll(B) == kTileBits) break;
+        }
+        for (int p = 0; p < nl && __builtin_popcountll(B) < kTileBits; ++p) B |= 1ull << p;
+        return B;
+    };
+    while (!remaining.empty()) {
+        std::uint64_t B = 0;
+        if (whole) {
+            B = (nl >= 64) ? ~0ull : ((1ull << nl) - 1);
+        } else {
+            int best = -1;
+            const std::size_t seeds = std::min<std::size_t>(kSeeds, remaining.size());
+            for (std::size_t sd = 0; sd < seeds; ++sd) {
+                const std::uint64_t cand = candidate(sd);
+                const int got = take(cand, nullptr, nullptr);
+                if (got > best) {
+                    best = got;
+                    B = cand;
+                }
+            }
+        }
+        Pass ps;
+        std::vector<int> keep;
+        keep.reserve(remaining.size());
+        take(B, &ps, &keep);
         if (ps.ops.empty()) fail(QRT_ERR_INVALID, "gate planner made no progress");
         if (!ps.wide) {
             for (int p = 0; p < nl; ++p)

@@ -55,6 +55,7 @@ struct PGroup {
     int nd;       // |D|
     int dpos[kMaxDiffBits];
     int need;     // bit 0: some term reads Re(w), bit 1: some term reads Im(w)
+    int real;     // every coefficient of the group is real (imaginary part exactly 0)
 };
 
 struct PPass {
@@ -126,6 +127,104 @@ __device__ __forceinline__ double2 group_pairs(const double2* __restrict__ tile,
         }
     }
     return acc;
+}
+
+// Fast path when the canonical bit h >= 5: the low five tile bits of the
+// canonical element are the lane id, everything else depends only on the
+// (warp-uniform) iteration index, so signs, table index bits and addresses
+// split into a per-lane constant and a uniform part computed once per step.
+template <int NEED, int ND, bool REAL>
+__device__ __forceinline__ double2 group_pairs_lane(const double2* __restrict__ tile, const PGroup& G,
+                                                    const double4* __restrict__ tbl, int half, int lane) {
+    double acx[4] = {0.0, 0.0, 0.0, 0.0}, acy[4] = {0.0, 0.0, 0.0, 0.0};
+    const int X = G.xy_tile, h = G.hbit, m0 = G.m0_tile;
+    const int E = half << 1;
+    // table-index bits split into lane bits (tile bits < 5) and uniform bits
+    int lane_k = 0, DH = 0;
+#pragma unroll
+    for (int i = 0; i < ND; ++i) {
+        const int b = G.dpos[i];
+        if (b < 5)
+            lane_k |= ((lane >> b) & 1) << i;
+        else
+            DH |= 1 << b;
+    }
+    const int lane_par = __popc(lane & m0) & 1;
+    const double2* __restrict__ tb = tile + lane;
+    const double2* __restrict__ ta = tile + (lane ^ (X & 31));
+    const int Xhi = X & ~31;
+    const int free = ((E - 1) & ~31) & ~(1 << h) & ~DH;  // enumerated uniformly
+    int s = 0;
+    do {  // each pattern of the uniform table-index bits
+        int k = lane_k;
+#pragma unroll
+        for (int i = 0; i < ND; ++i) {
+            const int b = G.dpos[i];
+            if (b >= 5) k |= ((s >> b) & 1) << i;
+        }
+        const double4 cf = tbl[k];
+        // all uniform parts with that pattern (ascending submasks of `free`),
+        // four at a time into independent accumulators
+        auto pair_val = [&](int ehi, double& re_out, double& im_out) {
+            const int odd = lane_par ^ (__popc(ehi & m0) & 1);
+            const double2 b = tb[ehi];
+            const double2 a = ta[ehi ^ Xhi];
+            if (NEED & 1) re_out = flip_if(fma(a.x, b.x, a.y * b.y), odd);
+            if (NEED & 2) im_out = flip_if(fma(a.x, b.y, -a.y * b.x), odd);
+        };
+        int f = 0;
+        if (__popc(free) >= 2) {
+            do {
+                const int f1 = (f - free) & free, f2 = (f1 - free) & free, f3 = (f2 - free) & free;
+                double r[4] = {0.0, 0.0, 0.0, 0.0}, q[4] = {0.0, 0.0, 0.0, 0.0};
+                pair_val(s | f, r[0], q[0]);
+                pair_val(s | f1, r[1], q[1]);
+                pair_val(s | f2, r[2], q[2]);
+                pair_val(s | f3, r[3], q[3]);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (NEED & 1) {
+                        acx[u] = fma(cf.x, r[u], acx[u]);
+                        if (!REAL) acy[u] = fma(cf.y, r[u], acy[u]);
+                    }
+                    if (NEED & 2) {
+                        acx[u] = fma(cf.z, q[u], acx[u]);
+                        if (!REAL) acy[u] = fma(cf.w, q[u], acy[u]);
+                    }
+                }
+                f = (f3 - free) & free;
+            } while (f != 0);
+        } else {
+            do {
+                double r = 0.0, q = 0.0;
+                pair_val(s | f, r, q);
+                if (NEED & 1) {
+                    acx[0] = fma(cf.x, r, acx[0]);
+                    if (!REAL) acy[0] = fma(cf.y, r, acy[0]);
+                }
+                if (NEED & 2) {
+                    acx[0] = fma(cf.z, q, acx[0]);
+                    if (!REAL) acy[0] = fma(cf.w, q, acy[0]);
+                }
+                f = (f - free) & free;
+            } while (f != 0);
+        }
+        s = (s - DH) & DH;
+    } while (s != 0);
+    return make_double2((acx[0] + acx[1]) + (acx[2] + acx[3]), (acy[0] + acy[1]) + (acy[2] + acy[3]));
+}
+
+template <int NEED, bool REAL>
+__device__ __forceinline__ double2 group_pairs_nd(const double2* __restrict__ tile, const PGroup& G,
+                                                  const double4* __restrict__ tbl, int half, int lane) {
+    switch (G.nd) {
+        case 0: return group_pairs_lane<NEED, 0, REAL>(tile, G, tbl, half, lane);
+        case 1: return group_pairs_lane<NEED, 1, REAL>(tile, G, tbl, half, lane);
+        case 2: return group_pairs_lane<NEED, 2, REAL>(tile, G, tbl, half, lane);
+        case 3: return group_pairs_lane<NEED, 3, REAL>(tile, G, tbl, half, lane);
+        case 4: return group_pairs_lane<NEED, 4, REAL>(tile, G, tbl, half, lane);
+        default: return group_pairs<NEED>(tile, G, tbl, half, lane);
+    }
 }
 
 __global__ void __launch_bounds__(kThreads, 2)
@@ -203,10 +302,24 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         __syncwarp();
         double2 g;
-        switch (G.need) {
-            case 1: g = group_pairs<1>(tile, G, tbl, half, lane); break;
-            case 2: g = group_pairs<2>(tile, G, tbl, half, lane); break;
-            default: g = group_pairs<3>(tile, G, tbl, half, lane); break;
+        if (G.hbit < 5 || half < 32) {
+            switch (G.need) {
+                case 1: g = group_pairs<1>(tile, G, tbl, half, lane); break;
+                case 2: g = group_pairs<2>(tile, G, tbl, half, lane); break;
+                default: g = group_pairs<3>(tile, G, tbl, half, lane); break;
+            }
+        } else if (G.real) {
+            switch (G.need) {
+                case 1: g = group_pairs_nd<1, true>(tile, G, tbl, half, lane); break;
+                case 2: g = group_pairs_nd<2, true>(tile, G, tbl, half, lane); break;
+                default: g = group_pairs_nd<3, true>(tile, G, tbl, half, lane); break;
+            }
+        } else {
+            switch (G.need) {
+                case 1: g = group_pairs_nd<1, false>(tile, G, tbl, half, lane); break;
+                case 2: g = group_pairs_nd<2, false>(tile, G, tbl, half, lane); break;
+                default: g = group_pairs_nd<3, false>(tile, G, tbl, half, lane); break;
+            }
         }
         acc.x += g.x;
         acc.y += g.y;
@@ -380,12 +493,16 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
             std::size_t at = 0;
             while (at < members.size()) {
                 const int t0 = members[at];
-                const int m0 = compress_bits((z[t0] | y[t0]) & ps.B, h.tile_pos, T);
+                const int xt = compress_bits(xy, h.tile_pos, T);
+                // the canonical bit (top bit of the flip mask) is 0 in every visited
+                // element, so sign-mask bits there never matter: drop them
+                const int hmask = 1 << (31 - __builtin_clz(static_cast<unsigned>(xt)));
+                const int m0 = compress_bits((z[t0] | y[t0]) & ps.B, h.tile_pos, T) & ~hmask;
                 int D = 0;
                 std::size_t end = at;
                 while (end < members.size()) {
                     const int t = members[end];
-                    const int d = compress_bits((z[t] | y[t]) & ps.B, h.tile_pos, T) ^ m0;
+                    const int d = (compress_bits((z[t] | y[t]) & ps.B, h.tile_pos, T) & ~hmask) ^ m0;
                     if (popc(static_cast<std::uint64_t>(D | d)) > kMaxDiffBits) break;
                     D |= d;
                     ++end;
@@ -400,6 +517,7 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
                 G.t_begin = static_cast<int>(dterms.size());
                 G.t_count = static_cast<int>(end - at);
                 G.need = 0;
+                G.real = 1;
                 for (std::size_t q = at; q < end; ++q) {
                     const int t = members[q];
                     const int ycnt = popc(y[t]);
@@ -408,12 +526,13 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
                     tm.m = (z[t] | y[t]) & ~ps.B;  // outer parity: bits outside the tile only
                     tm.gz = gz[t];
                     tm.f = make_double2(sgn * coeffs[2 * t], sgn * coeffs[2 * t + 1]);
-                    const int d = compress_bits((z[t] | y[t]) & ps.B, h.tile_pos, T) ^ m0;
+                    const int d = (compress_bits((z[t] | y[t]) & ps.B, h.tile_pos, T) & ~hmask) ^ m0;
                     int dk = 0;
                     for (int i = 0; i < G.nd; ++i) dk |= ((d >> G.dpos[i]) & 1) << i;
                     tm.dk = dk;
                     tm.comp = ycnt & 1;
                     G.need |= tm.comp ? 2 : 1;
+                    if (coeffs[2 * t + 1] != 0.0) G.real = 0;
                     dterms.push_back(tm);
                 }
                 dgroups.push_back(G);

@@ -33,7 +33,10 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 HBM_PEAK_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
-FP64_PEAK_NOMINAL = 37.0    # TFLOP/s, HGX B200 datasheet (296 TF / 8); not in MEASURED_PEAKS.json
+# FP64 tensor (DMMA) peak measured on this pool's B200s by tools/microbench_fp64.cu
+# (profiles/r1_microbench_fp64.txt: 37.0 TFLOP/s; datasheet 296 TF / 8 = 37).  MEASURED_PEAKS.json
+# only carries bf16, which is not the gate kernel's arithmetic.
+FP64_TENSOR_PEAK = 37.0
 
 
 def parse():
@@ -43,7 +46,12 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--qubits", type=int, default=30)
-    ap.add_argument("--layers", type=int, default=0, help="default 4n (PAPER.md:958)")
+    ap.add_argument("--circuit", choices=["gatefabric", "hea"], default="gatefabric",
+                    help="gatefabric (C2/C3) or the hardware-efficient ansatz (C4)")
+    ap.add_argument("--layers", type=int, default=0, help="default 4n for GateFabric (PAPER.md:958), 20 for HEA")
+    ap.add_argument("--hamiltonian", choices=["jw", "uniform"], default="jw",
+                    help="jw: gen_synthetic_jw(n,1,span); uniform: --terms random words (C5 stress)")
+    ap.add_argument("--terms", type=int, default=10000)
     ap.add_argument("--span", type=int, default=10)
     ap.add_argument("--schedule", choices=["flat", "hierarchical", "adhoc"], default="flat")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -104,47 +112,75 @@ def dist_env():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
+def uniform_terms(qb, n, count, seed=2024):
+    """C5 stress Hamiltonian: letters "IXYZ"[u], coefficients
+    U(-1, 1), from numpy's PCG64(2024) (the reference has no such generator)."""
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    letters = rng.integers(0, 4, size=(count, n))
+    coeffs = rng.uniform(-1.0, 1.0, size=count)
+    return [qb.PauliTerm(complex(c, 0.0), "".join("IXYZ"[v] for v in row)) for row, c in zip(letters, coeffs)]
+
+
 def workload(qb, args, p):
     n = args.qubits
-    layers = args.layers or 4 * n
-    circuit = qb.gen_gatefabric(n, layers, 1, True)
+    if args.circuit == "hea":
+        layers = args.layers or 20
+        circuit = qb.gen_hea(n, layers, 1, True)
+    else:
+        layers = args.layers or 4 * n
+        circuit = qb.gen_gatefabric(n, layers, 1, True)
     deps = qb.build_dependency_graph(circuit)
     shape = qb.ClusterShape.flat(p)
     sched = {"flat": qb.flat_tiling, "hierarchical": qb.hierarchical_tiling, "adhoc": qb.adhoc_schedule}[args.schedule](
         circuit, deps, shape)
-    terms = qb.gen_synthetic_jw(n, 1, args.span)
+    terms = qb.gen_synthetic_jw(n, 1, args.span) if args.hamiltonian == "jw" else uniform_terms(qb, n, args.terms)
     plan = qb.plan_evc(terms, n, shape, True, 8)
     return n, layers, circuit, sched, terms, plan, shape
 
 
 def config_of(args, n, layers, n_gates, n_terms, p, qr_qsu=None, qr_evc=None):
-    return {"workload": f"C2 GateFabric {n}q layers={layers} ({n_gates} dense 4q gates, seed 1) + EVC of "
-                        f"gen_synthetic_jw({n},1,max_span={args.span}) ({n_terms} Pauli strings), {args.schedule} "
-                        f"schedule, p={p}",
+    circ = (f"C2 GateFabric {n}q layers={layers} ({n_gates} dense 4q gates, seed 1)" if args.circuit == "gatefabric"
+            else f"C4 HEA {n}q depth={layers} ({n_gates} gates: RY dense, RZ/CZ diagonal, seed 1)")
+    ham = (f"gen_synthetic_jw({n},1,max_span={args.span})" if args.hamiltonian == "jw"
+           else f"uniform random words (PCG64 2024)")
+    return {"workload": f"{circ} + EVC of {ham} ({n_terms} Pauli strings), {args.schedule} schedule, p={p}",
             "qubits": n, "pes": p, "schedule": args.schedule, "qr_qsu": qr_qsu, "qr_evc": qr_evc,
             "l2": "inputs larger than L2 (state 16 B x 2^n)", "parallelism": f"state sharded {p}-way"}
 
 
 def cpu_baseline(args, n, p, n_gates, n_terms, layers):
     """Reference CPU path (oracle/_ref, the unmodified reference) on a bounded
-    sample: n_s-qubit state, 6 gates + 24 strings, scaled linearly in 2^n."""
+    sample: an n_s-qubit state, the first gates of the circuit (6 GateFabric
+    blocks, or one HEA layer) + 24 strings, scaled linearly in 2^n."""
     from oracle import ref as R
 
     if not R.available():
         return None
     import multiprocessing
 
+    import paper_2410_04252_b200 as qb
+
     ns = min(args.cpu_sample_qubits, n)
     workers = min(p, multiprocessing.cpu_count())
-    circ = R.Circuit.gatefabric(ns, 4, 1, True)
-    terms = R.Terms.jw(ns, 1, args.span)
+    if args.circuit == "hea":
+        circ = R.Circuit.from_product(qb.gen_hea(ns, 1, 1, True))
+        n_sample = 3 * ns - 1
+    else:
+        circ = R.Circuit.gatefabric(ns, 4, 1, True)
+        n_sample = 6
+    if args.hamiltonian == "jw":
+        terms = R.Terms.jw(ns, 1, args.span)
+    else:
+        terms = R.Terms.from_product(uniform_terms(qb, ns, 64), ns)
     t0 = time.time()
-    g, t = R.time_sample(circ, terms, p, workers, 6, 24)
+    g, t = R.time_sample(circ, terms, p, workers, n_sample, 24)
     wall = time.time() - t0
     scale = float(1 << (n - ns))
     per_iter = (g * n_gates + t * n_terms) * scale
     return {"value": per_iter, "unit": "s", "cores": workers, "kind": "reference",
-            "sample": f"reference dist_sim (oracle/_ref) apply_gate_narrow x6 + expectation x24 strings at "
+            "sample": f"reference dist_sim (oracle/_ref) apply_gate_narrow x{n_sample} + expectation x24 strings at "
                       f"n={ns}, p={p}, workers={workers} ({wall:.1f} s of CPU work); per-gate {g:.3g} s and "
                       f"per-string {t:.3g} s scaled by 2^{n - ns} to {n_gates} gates + {n_terms} strings "
                       f"(extrapolated, linear in 2^n)"}
@@ -160,8 +196,12 @@ def run_reference(args):
     p = max(1, world)
     n = args.qubits
     layers = args.layers or 4 * n
-    n_gates = qb.gatefabric_block_count(n, layers)
-    n_terms = int(qb.synthetic_jw_term_count(n, args.span))
+    if args.circuit == "hea":
+        layers = args.layers or 20
+        n_gates = layers * (3 * n - 1)
+    else:
+        n_gates = qb.gatefabric_block_count(n, layers)
+    n_terms = int(qb.synthetic_jw_term_count(n, args.span)) if args.hamiltonian == "jw" else args.terms
     if not R.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libqrtile_ref.so not built"}))
         return 0
@@ -259,6 +299,13 @@ def run_ours(args):
     fp64 = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else None
     qr = stats["qr"]
     pa = stats["pauli"]
+    traffic = None
+    try:  # DRAM bytes per gate-pass launch from the committed `ncu --set full` capture
+        tr = json.loads((ROOT / "profiles" / "roofline_traffic.json").read_text())
+        if tr.get("qubits") == n and tr.get("pes") == p:
+            traffic = tr["gate_pass_kernel"]["dram_bytes_per_launch"]
+    except Exception:
+        traffic = None
     mat_bytes = sum(16 * (1 << (2 * op.arity())) for op in circuit.operators)
     term_bytes = 8 * 5 * n_terms
     d2h = 16 * p * max(1, len(plan.tiles))
@@ -273,11 +320,14 @@ def run_ours(args):
         "e2e": {"value": wall_t, "unit": "s", "h2d_bytes_per_step": mat_bytes + term_bytes, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches // max(1, args.steps),
         "clocks": clk,
-        "roofline": {"bound": "hbm", "kernel": "gate_pass_kernel (QSU)", "achieved": achieved, "peak": hbm_peak,
-                     "unit": "GB/s", "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
-                     "peak_kind": peak_kind, "avg_launch_ms": gate_ms, "algorithmic_bytes_per_launch": gate_bytes,
-                     "fp64_tflops": fp64, "fp64_peak_nominal": FP64_PEAK_NOMINAL,
-                     "fp64_frac": (fp64 / FP64_PEAK_NOMINAL) if fp64 else None},
+        "roofline": {"bound": "tensor", "kernel": "gate_pass_kernel (QSU; DMMA fp64 tensor path)",
+                     "achieved": fp64, "peak": FP64_TENSOR_PEAK, "unit": "TFLOP/s",
+                     "frac": (fp64 / FP64_TENSOR_PEAK) if fp64 else None, "traffic": traffic,
+                     "peak_kind": "measured fp64 DMMA (tools/microbench_fp64.cu)",
+                     "avg_launch_ms": gate_ms, "algorithmic_bytes_per_launch": gate_bytes,
+                     "algorithmic_flops_per_launch": g["flops"] / max(1, g["launches"]),
+                     "hbm": {"achieved_gbs": achieved, "peak_gbs": hbm_peak, "peak_kind": peak_kind,
+                             "frac": (achieved / hbm_peak) if achieved else None}},
         "phases_ms": {"gates": g["ms"], "qr": qr["ms"], "pauli": pa["ms"], "misc": stats["misc"]["ms"],
                       "gate_passes": g["launches"], "qr_launches": qr["launches"], "pauli_passes": pa["launches"],
                       "qr_nvlink_gbs": (qr["bytes"] / (qr["ms"] / 1e3) / 1e9) if qr["ms"] > 0 else None},

@@ -333,6 +333,50 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
 }
 
+// Flip masks too wide for a shared-memory tile: the canonical pairs are read
+// straight from HBM (both partners), one group per grid-stride sweep.  Used
+// for generic Pauli words (e.g. uniformly random strings); Jordan-Wigner
+// words always take the tiled kernel above.
+struct WGroup {
+    std::uint64_t x;      // flip mask, local positions
+    int hbit;             // canonical bit
+    int t_begin, t_count;
+};
+
+__global__ void __launch_bounds__(256) pauli_wide_kernel(PePtrsP ptrs, int nl, int pe_begin, const WGroup* __restrict__ groups,
+                                                         int n_groups, const PTerm* __restrict__ terms,
+                                                         double* __restrict__ red) {
+    __shared__ double2 scratch[8];
+    const amp_t* __restrict__ v = ptrs.p[blockIdx.y];
+    const std::uint64_t pe = static_cast<std::uint64_t>(pe_begin) + blockIdx.y;
+    const std::uint64_t half = 1ull << (nl - 1);
+    double2 acc = make_double2(0.0, 0.0);
+    for (int gi = 0; gi < n_groups; ++gi) {
+        const WGroup G = groups[gi];
+        for (std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; idx < half;
+             idx += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+            const std::uint64_t e = ((idx >> G.hbit) << (G.hbit + 1)) | (idx & ((1ull << G.hbit) - 1));
+            const double2 a = v[e ^ G.x];
+            const double2 b = v[e];
+            const double re = fma(a.x, b.x, a.y * b.y);
+            const double im = fma(a.x, b.y, -a.y * b.x);
+            for (int t = 0; t < G.t_count; ++t) {
+                const PTerm tm = terms[G.t_begin + t];
+                const int odd = (__popcll(e & tm.m) + __popcll(pe & tm.gz)) & 1;
+                const double val = flip_if(tm.comp ? im : re, odd);
+                acc.x = fma(tm.f.x, val, acc.x);
+                acc.y = fma(tm.f.y, val, acc.y);
+            }
+        }
+    }
+    const double2 tot = block_sum(acc, scratch);
+    if (threadIdx.x == 0) {
+        double* slot = red + 2 * (static_cast<std::size_t>(blockIdx.y) * gridDim.x + blockIdx.x);
+        slot[0] += tot.x;
+        slot[1] += tot.y;
+    }
+}
+
 // Deterministic per-PE reduction of `count` slots of (re, im).
 __global__ void __launch_bounds__(256) reduce_slots_kernel(const double* __restrict__ red, int count, double* out) {
     __shared__ double2 scratch[8];
@@ -409,18 +453,21 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
     // ---- group by flip mask -------------------------------------------------
     std::map<std::uint64_t, std::vector<int>> by_xy;
     for (int t = 0; t < n_terms; ++t) by_xy[x[t] | y[t]].push_back(t);
+    const int T = std::min(kTileBits, nl);
+    const int coal = std::min(kCoalBits, nl);
+    const std::uint64_t coal_mask = (1ull << coal) - 1;
     std::vector<int> diag;
-    std::vector<std::pair<std::uint64_t, std::vector<int>>> flips;
+    std::vector<std::pair<std::uint64_t, std::vector<int>>> flips, wide;
     for (auto& kv : by_xy) {
         if (kv.first == 0)
             diag = kv.second;
+        else if (popc(kv.first | coal_mask) > T)
+            wide.emplace_back(kv.first, kv.second);
         else
             flips.emplace_back(kv.first, kv.second);
     }
 
     // ---- passes: tile positions covering many flip masks --------------------
-    const int T = std::min(kTileBits, nl);
-    const int coal = std::min(kCoalBits, nl);
     struct Pass {
         std::uint64_t B;
         std::vector<int> groups;  // indices into flips
@@ -542,13 +589,35 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
         h.g_count = static_cast<int>(dgroups.size()) - h.g_begin;
         hdrs.push_back(h);
     }
+    // wide flip masks: full-vector sweeps (terms keep their full sign masks)
+    std::vector<WGroup> wgroups;
+    for (const auto& [xy, members] : wide) {
+        WGroup W{};
+        W.x = xy;
+        W.hbit = 63 - __builtin_clzll(xy);
+        W.t_begin = static_cast<int>(dterms.size());
+        W.t_count = static_cast<int>(members.size());
+        for (int t : members) {
+            const int ycnt = popc(y[t]);
+            const double sgn = ((ycnt & 3) == 1 || (ycnt & 3) == 2) ? -2.0 : 2.0;
+            PTerm tm{};
+            tm.m = z[t] | y[t];
+            tm.gz = gz[t];
+            tm.f = make_double2(sgn * coeffs[2 * t], sgn * coeffs[2 * t + 1]);
+            tm.comp = ycnt & 1;
+            dterms.push_back(tm);
+        }
+        wgroups.push_back(W);
+    }
     const std::size_t gbytes = dgroups.size() * sizeof(PGroup);
     const std::size_t toff = (gbytes + 255) & ~std::size_t{255};
-    const std::size_t total = toff + dterms.size() * sizeof(PTerm) + 16;
+    const std::size_t woff = (toff + dterms.size() * sizeof(PTerm) + 255) & ~std::size_t{255};
+    const std::size_t total = woff + wgroups.size() * sizeof(WGroup) + 16;
     char* host = static_cast<char*>(ensure_pinned(st, total));
     QRT_CUDA(cudaStreamSynchronize(st->stream));
     std::memcpy(host, dgroups.data(), gbytes);
     std::memcpy(host + toff, dterms.data(), dterms.size() * sizeof(PTerm));
+    std::memcpy(host + woff, wgroups.data(), wgroups.size() * sizeof(WGroup));
     char* dev = static_cast<char*>(ensure_ops(st, total));
     QRT_CUDA(cudaMemcpyAsync(dev, host, total, cudaMemcpyHostToDevice, st->stream));
 
@@ -577,6 +646,16 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
             QRT_CUDA(cudaGetLastError());
             st->stats[QRT_K_PAULI].launches++;
             st->stats[QRT_K_PAULI].bytes += 16.0 * static_cast<double>(st->amps) * st->pe_count;
+        }
+        if (!wgroups.empty()) {
+            dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(st->pe_count));
+            pauli_wide_kernel<<<grid, 256, 0, st->stream>>>(ptrs, nl, st->pe_begin,
+                                                            reinterpret_cast<const WGroup*>(dev + woff),
+                                                            static_cast<int>(wgroups.size()),
+                                                            reinterpret_cast<const PTerm*>(dev + toff), red);
+            QRT_CUDA(cudaGetLastError());
+            st->stats[QRT_K_PAULI].launches++;
+            st->stats[QRT_K_PAULI].bytes += 32.0 * static_cast<double>(st->amps) * st->pe_count * wgroups.size() / 2;
         }
         reduce_slots_kernel<<<st->pe_count, 256, 0, st->stream>>>(red, ctas, out);
         QRT_CUDA(cudaGetLastError());

@@ -302,3 +302,21 @@ def test_large_qr_roundtrip_and_norm(qb, device):
     for pe in range(p):
         assert np.array_equal(st.sub_of(pe), before[pe])
     assert abs(st.norm() - 1.0) <= 1e-12
+
+
+@pytest.mark.parametrize("n,p", [(16, 1), (16, 2), (18, 4)])
+def test_expectation_uniform_random_strings(qb, device, n, p):
+    """Uniformly random words (SURVEY §8d C5 stress): most flip masks are wider
+    than a shared-memory tile and take the full-vector path."""
+    rng = np.random.default_rng(2024 + n + p)
+    terms = []
+    for _ in range(60):
+        letters = "".join("IXYZ"[int(rng.integers(4))] for _ in range(n))
+        terms.append(qb.PauliTerm(complex(rng.uniform(-1, 1), rng.uniform(-0.1, 0.1)), letters))
+    psi = qb.random_state(n, 77 + n)
+    shape = qb.ClusterShape.flat(p)
+    plan = qb.plan_evc(terms, n, shape, True, 4)
+    st = qb.init_state_from(psi, shape)
+    got = qb.expectation(st, plan, terms)
+    want = oracle_expectation(qb, psi, n, p, terms, plan)
+    assert abs(got - want) <= E_TOL * (1 + abs(want)), (got, want)

@@ -70,7 +70,12 @@ qrt_status qrt_comm_destroy(qrt_comm* comm);
  * multiple of the world size and rank r owns PEs [r*p/w, (r+1)*p/w).
  * Collective when comm != NULL. */
 qrt_status qrt_state_create(int n, int p, int device, qrt_comm* comm, qrt_state** out);
+/* Releases the state.  Its device buffers are parked and reused by the next
+ * qrt_state_create of the same (n, p, device, comm) (a VQE loop creates one
+ * state per iteration); qrt_release_cache frees all parked states
+ * (collective when they were created with a communicator). */
 qrt_status qrt_state_destroy(qrt_state* st);
+qrt_status qrt_release_cache(void);
 qrt_status qrt_state_info(const qrt_state* st, int* n, int* p, int* pe_begin, int* pe_count);
 qrt_status qrt_state_set_zero(qrt_state* st);
 /* Copy one owned PE's 2^(n-g) amplitudes (position order) in / out. */
@@ -95,6 +100,13 @@ qrt_status qrt_apply_gates(qrt_state* st, int n_gates, const int* arity, const i
  * change PE over NVLink; collective when comm != NULL.  *relocated receives
  * the number of amplitudes (all PEs) whose owning PE changed. */
 qrt_status qrt_reorder(qrt_state* st, const int* dest, uint64_t* relocated);
+
+/* Host-only replay of qrt_reorder's index mapping (no device needed): for
+ * each of the 2^(n-g) amplitudes of source PE `src_pe`, the destination PE
+ * and offset the kernel stores it to.  Used to emulate and check the
+ * multi-process exchange on CPU. */
+qrt_status qrt_reorder_plan(int n, int p, const int* dest, int src_pe, uint64_t* dst_pe, uint64_t* dst_off,
+                            uint64_t* relocated);
 
 /* The per-PE accumulation of expectation() for one plan tile
  * (dist_sim.cpp:84-97, 289-295):

@@ -53,6 +53,43 @@ __global__ void zero_state_kernel(amp_t* __restrict__ v, std::uint64_t count, in
     for (; i < count; i += stride) v[i] = make_double2((set_first && i == 0) ? 1.0 : 0.0, 0.0);
 }
 
+// Parked states, reused by qrt_state_create with the same (n, p, device,
+// comm): a VQE loop creates one state per iteration (evaluate_energy,
+// dist_sim.cpp:357-363), and re-allocating tens of GiB plus re-opening IPC
+// peer mappings every iteration would dominate small steps.  Every rank
+// parks and reuses in the same order, so peer mappings stay valid.
+std::mutex g_cache_mu;
+std::vector<qrt_state*> g_cache;
+
+void free_state(qrt_state* st) {
+    DeviceGuard g(st->device);
+    if (st->stream) cudaStreamSynchronize(st->stream);
+    for (void* ptr : st->ipc_opened) cudaIpcCloseMemHandle(ptr);
+    for (int b = 0; b < 2; ++b)
+        for (auto* ptr : st->bufs[b])
+            if (ptr) cudaFree(ptr);
+    if (st->d_red) cudaFree(st->d_red);
+    if (st->d_ops) cudaFree(st->d_ops);
+    if (st->h_pinned) cudaFreeHost(st->h_pinned);
+    if (st->d_flag) cudaFree(st->d_flag);
+    if (st->ev0) cudaEventDestroy(st->ev0);
+    if (st->ev1) cudaEventDestroy(st->ev1);
+    if (st->stream) cudaStreamDestroy(st->stream);
+    delete st;
+}
+
+qrt_state* take_cached(int n, int p, int device, qrt_comm* comm) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (std::size_t i = 0; i < g_cache.size(); ++i) {
+        qrt_state* st = g_cache[i];
+        if (st->n == n && st->p == p && st->device == device && st->comm == comm) {
+            g_cache.erase(g_cache.begin() + static_cast<std::ptrdiff_t>(i));
+            return st;
+        }
+    }
+    return nullptr;
+}
+
 int grid_for(std::uint64_t items, int threads) {
     int sms = 148;
     std::uint64_t want = (items + threads - 1) / threads;
@@ -230,6 +267,20 @@ qrt_status qrt_state_create(int n, int p, int device, qrt_comm* comm, qrt_state*
         }
         require(device >= 0 && device < ndev, QRT_ERR_NO_DEVICE, "device index out of range");
         DeviceGuard dg(device);
+        if (qrt_state* cached = take_cached(n, p, device, comm)) {
+            // buffer parity is kept (peers address the same physical buffers)
+            cached->profile = false;
+            for (auto& sct : cached->stats) sct = qrt_kernel_stats{};
+            for (int i = 0; i < cached->pe_count; ++i)
+                zero_state_kernel<<<grid_for(cached->amps, 256), 256, 0, cached->stream>>>(
+                    cached->live(i), cached->amps, cached->pe_begin + i == 0);
+            QRT_CUDA(cudaGetLastError());
+            cached->stats[QRT_K_MISC].launches += static_cast<std::uint64_t>(cached->pe_count);
+            barrier_on_stream(cached);  // collective, like a fresh create
+            QRT_CUDA(cudaStreamSynchronize(cached->stream));
+            *out = cached;
+            return;
+        }
 
         auto st = new qrt_state;
         st->n = n;
@@ -302,7 +353,7 @@ qrt_status qrt_state_create(int n, int p, int device, qrt_comm* comm, qrt_state*
                 QRT_CUDA(cudaStreamSynchronize(st->stream));
             }
         } catch (...) {
-            qrt_state_destroy(st);
+            free_state(st);
             throw;
         }
         *out = st;
@@ -312,20 +363,23 @@ qrt_status qrt_state_create(int n, int p, int device, qrt_comm* comm, qrt_state*
 qrt_status qrt_state_destroy(qrt_state* st) {
     return guarded([&] {
         if (!st) return;
-        DeviceGuard g(st->device);
-        if (st->stream) cudaStreamSynchronize(st->stream);
-        for (void* ptr : st->ipc_opened) cudaIpcCloseMemHandle(ptr);
-        for (int b = 0; b < 2; ++b)
-            for (auto* ptr : st->bufs[b])
-                if (ptr) cudaFree(ptr);
-        if (st->d_red) cudaFree(st->d_red);
-        if (st->d_ops) cudaFree(st->d_ops);
-        if (st->h_pinned) cudaFreeHost(st->h_pinned);
-        if (st->d_flag) cudaFree(st->d_flag);
-        if (st->ev0) cudaEventDestroy(st->ev0);
-        if (st->ev1) cudaEventDestroy(st->ev1);
-        if (st->stream) cudaStreamDestroy(st->stream);
-        delete st;
+        {
+            DeviceGuard g(st->device);
+            QRT_CUDA(cudaStreamSynchronize(st->stream));
+        }
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        g_cache.push_back(st);  // parked; qrt_release_cache frees
+    });
+}
+
+qrt_status qrt_release_cache(void) {
+    return guarded([&] {
+        std::vector<qrt_state*> all;
+        {
+            std::lock_guard<std::mutex> lk(g_cache_mu);
+            all.swap(g_cache);
+        }
+        for (qrt_state* st : all) free_state(st);
     });
 }
 
@@ -396,6 +450,14 @@ qrt_status qrt_reorder(qrt_state* st, const int* dest, std::uint64_t* relocated)
         std::uint64_t moved = reorder(st, dest);
         QRT_CUDA(cudaStreamSynchronize(st->stream));
         if (relocated) *relocated = moved;
+    });
+}
+
+qrt_status qrt_reorder_plan(int n, int p, const int* dest, int src_pe, std::uint64_t* dst_pe, std::uint64_t* dst_off,
+                            std::uint64_t* relocated) {
+    return guarded([&] {
+        require(dest && dst_pe && dst_off, QRT_ERR_INVALID, "null argument");
+        reorder_plan(n, p, dest, src_pe, dst_pe, dst_off, relocated);
     });
 }
 

@@ -106,6 +106,8 @@ void barrier_on_stream(qrt_state* st);  // NCCL all-reduce of one int (no-op sin
 void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, const double* mats,
                  const unsigned* flags);
 std::uint64_t reorder(qrt_state* st, const int* dest);
+void reorder_plan(int n, int p, const int* dest, int src_pe, std::uint64_t* dst_pe, std::uint64_t* dst_off,
+                  std::uint64_t* relocated);
 void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const std::uint64_t* y,
                        const std::uint64_t* z, const std::uint64_t* gz, const double* coeffs, double* partial);
 double norm(qrt_state* st);

@@ -105,6 +105,12 @@ void apply_gates_narrow(DistributedState& state, const Circuit& circuit, const s
 
 std::uint64_t perform_qr(DistributedState& state, const QrEvent& event);
 
+// The device-side position permutation perform_qr issues for `event` given the
+// current physical layout (qubit -> physical position): returns dest[p] for
+// qrt_reorder and the new physical layout.  Exposed for tests / ABI callers.
+std::vector<int> physical_reorder_plan(const QrEvent& event, const std::vector<int>& phys_pos_of,
+                                       std::vector<int>& new_phys_pos_of);
+
 void run_qsu(DistributedState& state, const Circuit& circuit, const Schedule& schedule, int workers = 1);
 
 double diag_expectation_term(const DistributedState& state, const PauliTerm& term);

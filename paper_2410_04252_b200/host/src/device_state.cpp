@@ -79,9 +79,10 @@ Masked mask_term(const PauliTerm& term, const DistributedState& st) {
 // except that departing slots below 2^4 are refilled by the highest staying
 // qubit (which moves down) and the arriving qubit goes to that high slot, so
 // both sides of the exchange move runs of >= 16 contiguous amplitudes.
-std::vector<int> physical_plan(const DistributedState& st, const QrEvent& ev, std::vector<int>& new_phys) {
-    const int n = st.n, nl = st.layout.n_local;
-    const std::vector<int>& phys = st.device->phys_pos_of;
+std::vector<int> physical_plan_impl(const QrEvent& ev, const std::vector<int>& phys, std::vector<int>& new_phys) {
+    const int n = ev.before.n, nl = ev.before.n_local;
+    std::vector<int> phys_qubit_at(static_cast<std::size_t>(n));
+    for (int q = 0; q < n; ++q) phys_qubit_at[static_cast<std::size_t>(phys[static_cast<std::size_t>(q)])] = q;
     constexpr int kLowRun = 4;
     new_phys.assign(static_cast<std::size_t>(n), -1);
     std::vector<int> arriving, freed;
@@ -117,7 +118,7 @@ std::vector<int> physical_plan(const DistributedState& st, const QrEvent& ev, st
             slots.push_back(f);
             continue;
         }
-        const int mover = st.device->phys_qubit_at[static_cast<std::size_t>(hi)];
+        const int mover = phys_qubit_at[static_cast<std::size_t>(hi)];
         new_phys[static_cast<std::size_t>(mover)] = f;
         taken[static_cast<std::size_t>(hi)] = 0;
         taken[static_cast<std::size_t>(f)] = 1;
@@ -130,6 +131,10 @@ std::vector<int> physical_plan(const DistributedState& st, const QrEvent& ev, st
     for (int q = 0; q < n; ++q)
         dest[static_cast<std::size_t>(phys[static_cast<std::size_t>(q)])] = new_phys[static_cast<std::size_t>(q)];
     return dest;
+}
+
+std::vector<int> physical_plan(const DistributedState& st, const QrEvent& ev, std::vector<int>& new_phys) {
+    return physical_plan_impl(ev, st.device->phys_pos_of, new_phys);
 }
 
 // Logical offset (reference position order) <-> physical offset inside a PE.
@@ -193,6 +198,11 @@ void submit_gates(DistributedState& st, const std::vector<const Operator*>& gate
 
 }  // namespace
 
+std::vector<int> physical_reorder_plan(const QrEvent& event, const std::vector<int>& phys_pos_of,
+                                       std::vector<int>& new_phys_pos_of) {
+    return physical_plan_impl(event, phys_pos_of, new_phys_pos_of);
+}
+
 // ---------------------------------------------------------------- context
 
 void init_device(int rank, int world, int device, const std::string& unique_id) {
@@ -218,6 +228,7 @@ std::string device_unique_id() {
 const DeviceContext& device_context() { return g_ctx; }
 
 void shutdown_device() {
+    qrt_release_cache();
     if (g_ctx.comm) qrt_comm_destroy(g_ctx.comm);
     g_ctx = DeviceContext{};
 }

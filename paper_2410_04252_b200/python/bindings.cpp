@@ -342,6 +342,11 @@ PYBIND11_MODULE(_qrtile, m) {
     m.def("apply_gate_narrow", &apply_gate_narrow, py::arg("state"), py::arg("gate"), py::arg("workers") = 1);
     m.def("apply_gates_narrow", &apply_gates_narrow);
     m.def("perform_qr", &perform_qr);
+    m.def("physical_reorder_plan", [](const QrEvent& ev, const std::vector<int>& phys) {
+        std::vector<int> np;
+        std::vector<int> dest = physical_reorder_plan(ev, phys, np);
+        return py::make_tuple(dest, np);
+    });
     m.def("run_qsu", &run_qsu, py::arg("state"), py::arg("circuit"), py::arg("schedule"), py::arg("workers") = 1);
     m.def("diag_expectation_term", &diag_expectation_term);
     m.def("expectation", &expectation, py::arg("state"), py::arg("plan"), py::arg("terms"), py::arg("workers") = 1);

@@ -1,0 +1,117 @@
+"""N>1 host logic on CPU: two gloo ranks (one per "GPU") emulate the
+distributed QR exactly as libqrt performs it — PE ownership (rank r owns PEs
+[r*p/w, (r+1)*p/w)), the physical placement chosen by physical_reorder_plan,
+and the kernel's own destination mapping replayed by qrt_reorder_plan — and
+exchange amplitudes with torch.distributed.  Results must equal the oracle's
+perform_qr (dist_sim.cpp:203-240) bit for bit, and relocation counts must
+equal qr_data_volume.
+"""
+import ctypes as C
+import os
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _plan(lib, n, p, dest, pe):
+    per = 1 << (n - (p.bit_length() - 1))
+    dpe = np.zeros(per, dtype=np.uint64)
+    doff = np.zeros(per, dtype=np.uint64)
+    rel = C.c_uint64()
+    rc = lib.qrt_reorder_plan(n, p, (C.c_int * n)(*dest), pe, dpe.ctypes.data_as(C.POINTER(C.c_uint64)),
+                              doff.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(rel))
+    assert rc == 0
+    return dpe, doff, rel.value
+
+
+def _worker(rank, world, port, n, p, seed, q):
+    sys.path.insert(0, str(ROOT))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    import paper_2410_04252_b200 as qb
+    from oracle import cpu
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lib = qb.load_libqrt()
+    per_rank = p // world
+    mine = list(range(rank * per_rank, (rank + 1) * per_rank))
+    psi = qb.random_state(n, seed)
+    sub_all = psi.reshape(p, -1).copy()           # oracle copy (every rank)
+    local = {pe: sub_all[pe].copy() for pe in mine}  # this rank's PEs, physical order
+    layout = qb.QubitLayout.identity(n, qb.ClusterShape.flat(p))
+    phys = list(range(n))
+    olay = cpu.Layout(n, p)
+    rng = np.random.default_rng(seed)
+    ok = True
+    for _ in range(4):
+        locals_ = 0
+        while bin(locals_).count("1") < layout.n_local:
+            locals_ |= 1 << int(rng.integers(n))
+        ev = qb.make_qr_event(layout, locals_)
+        if ev is None:
+            continue
+        dest, new_phys = qb.physical_reorder_plan(ev, phys)
+        # emulate the push kernel: each local PE sends every amplitude to (dst_pe, dst_off)
+        outgoing = [[] for _ in range(world)]
+        rel_seen = None
+        for pe in mine:
+            dpe, doff, rel = _plan(lib, n, p, dest, pe)
+            rel_seen = rel
+            for r in range(world):
+                sel = (dpe // per_rank) == r
+                outgoing[r].append((dpe[sel], doff[sel], local[pe][sel]))
+        incoming = [None] * world
+        for r in range(world):
+            gathered = [None] * world
+            dist.all_gather_object(gathered, outgoing[r])
+            incoming[r] = gathered  # what every rank sends to rank r
+        fresh = {pe: np.zeros_like(local[pe]) for pe in mine}
+        for src_rank in range(world):
+            for dpe, doff, vals in incoming[rank][src_rank]:
+                for pe in mine:
+                    sel = dpe == pe
+                    fresh[pe][doff[sel].astype(np.int64)] = vals[sel]
+        local = fresh
+        moved = cpu.perform_qr(sub_all, olay.dest_for(ev.after.pos_of))
+        olay.adopt(ev.after.pos_of)
+        ok = ok and rel_seen == moved == qb.qr_data_volume(len(ev.swaps), n)
+        # compare in reference (logical) position order
+        nl = layout.n_local
+        layout = ev.after
+        phys = new_phys
+        lp = [phys[layout.qubit_at[pos]] for pos in range(nl)]
+        idx = np.zeros(1 << nl, dtype=np.int64)
+        for pos, ph in enumerate(lp):
+            idx |= ((np.arange(1 << nl) >> pos) & 1) << ph
+        for pe in mine:
+            ok = ok and np.array_equal(local[pe][idx], sub_all[pe])
+    q.put((rank, bool(ok)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,p,seed", [(8, 2, 1), (10, 4, 2), (11, 8, 3)])
+def test_two_rank_reorder_matches_oracle(n, p, seed):
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, p, seed, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    results = dict(q.get(timeout=240) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+    assert results == {0: True, 1: True}

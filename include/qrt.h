@@ -118,6 +118,13 @@ qrt_status qrt_pauli_expectation(qrt_state* st, int n_terms, const uint64_t* x, 
                                  const uint64_t* z, const uint64_t* gz, const double* coeffs,
                                  double* partial);
 
+/* Host-only: the EVC pass plan qrt_pauli_expectation would build for these
+ * masks on a PE of n_local positions (passes, flip-mask groups, full-vector
+ * groups, planning seconds).  No device needed. */
+qrt_status qrt_pauli_plan_info(int n_local, int n_terms, const uint64_t* x, const uint64_t* y, const uint64_t* z,
+                               const uint64_t* gz, const double* coeffs, int* passes, int* groups, int* wide_groups,
+                               double* seconds);
+
 /* sqrt(sum |amp|^2) over all PEs (DistributedState::norm, dist_sim.cpp:115). */
 qrt_status qrt_norm(qrt_state* st, double* out);
 

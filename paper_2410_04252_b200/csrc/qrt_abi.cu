@@ -6,8 +6,13 @@
 // (dist_sim.cpp:122-131); upload/download <- init_state(ref)/flatten
 // (:133-161, position order); qrt_norm <- DistributedState::norm (:115-120).
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+
+#include <unistd.h>
 
 #include "qrt_internal.h"
 
@@ -15,6 +20,42 @@ namespace qrt {
 
 namespace {
 thread_local std::string g_last_error;
+
+// QRT_TRACE=<path>: every traced ABI call appends "name t_begin_us t_end_us"
+// (host wall clock, process-relative) — the host side of the timeline.
+struct Tracer {
+    std::FILE* f = nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    std::mutex mu;
+    Tracer() {
+        if (const char* path = std::getenv("QRT_TRACE")) {
+            std::string name = std::string(path) + "." + std::to_string(static_cast<long>(getpid()));
+            f = std::fopen(name.c_str(), "w");
+        }
+    }
+    ~Tracer() {
+        if (f) std::fclose(f);
+    }
+    double now_us() const {
+        return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    }
+};
+Tracer& tracer() {
+    static Tracer t;
+    return t;
+}
+struct TraceScope {
+    const char* name;
+    double b;
+    explicit TraceScope(const char* n) : name(n), b(tracer().f ? tracer().now_us() : 0.0) {}
+    ~TraceScope() {
+        Tracer& t = tracer();
+        if (!t.f) return;
+        std::lock_guard<std::mutex> lk(t.mu);
+        std::fprintf(t.f, "%s %.1f %.1f\n", name, b, t.now_us());
+        std::fflush(t.f);
+    }
+};
 
 template <class F>
 qrt_status guarded(F&& f) {
@@ -250,6 +291,7 @@ qrt_status qrt_comm_destroy(qrt_comm* comm) {
 }
 
 qrt_status qrt_state_create(int n, int p, int device, qrt_comm* comm, qrt_state** out) {
+    TraceScope trace_("qrt_state_create");
     return guarded([&] {
         require(out != nullptr, QRT_ERR_INVALID, "null out");
         require(p >= 1 && (p & (p - 1)) == 0, QRT_ERR_CONFIG, "p must be a power of two");
@@ -361,6 +403,7 @@ qrt_status qrt_state_create(int n, int p, int device, qrt_comm* comm, qrt_state*
 }
 
 qrt_status qrt_state_destroy(qrt_state* st) {
+    TraceScope trace_("qrt_state_destroy");
     return guarded([&] {
         if (!st) return;
         {
@@ -407,6 +450,7 @@ qrt_status qrt_state_set_zero(qrt_state* st) {
 }
 
 qrt_status qrt_state_upload(qrt_state* st, int pe, const double* amps) {
+    TraceScope trace_("qrt_state_upload");
     return guarded([&] {
         require(st && amps, QRT_ERR_INVALID, "null argument");
         require(pe >= st->pe_begin && pe < st->pe_begin + st->pe_count, QRT_ERR_INVALID, "PE not owned by this process");
@@ -418,6 +462,7 @@ qrt_status qrt_state_upload(qrt_state* st, int pe, const double* amps) {
 }
 
 qrt_status qrt_state_download(const qrt_state* st, int pe, double* amps) {
+    TraceScope trace_("qrt_state_download");
     return guarded([&] {
         require(st && amps, QRT_ERR_INVALID, "null argument");
         require(pe >= st->pe_begin && pe < st->pe_begin + st->pe_count, QRT_ERR_INVALID, "PE not owned by this process");
@@ -430,6 +475,7 @@ qrt_status qrt_state_download(const qrt_state* st, int pe, double* amps) {
 
 qrt_status qrt_apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, const double* mats,
                            const unsigned* flags) {
+    TraceScope trace_("qrt_apply_gates");
     return guarded([&] {
         require(st != nullptr, QRT_ERR_INVALID, "null state");
         if (n_gates == 0) return;
@@ -443,6 +489,7 @@ qrt_status qrt_apply_gates(qrt_state* st, int n_gates, const int* arity, const i
 }
 
 qrt_status qrt_reorder(qrt_state* st, const int* dest, std::uint64_t* relocated) {
+    TraceScope trace_("qrt_reorder");
     return guarded([&] {
         require(st && dest, QRT_ERR_INVALID, "null argument");
         DeviceGuard g(st->device);
@@ -464,6 +511,7 @@ qrt_status qrt_reorder_plan(int n, int p, const int* dest, int src_pe, std::uint
 qrt_status qrt_pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const std::uint64_t* y,
                                  const std::uint64_t* z, const std::uint64_t* gz, const double* coeffs,
                                  double* partial) {
+    TraceScope trace_("qrt_pauli_expectation");
     return guarded([&] {
         require(st && partial, QRT_ERR_INVALID, "null argument");
         require(n_terms == 0 || (x && y && z && gz && coeffs), QRT_ERR_INVALID, "null term arrays");
@@ -473,7 +521,18 @@ qrt_status qrt_pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t
     });
 }
 
+qrt_status qrt_pauli_plan_info(int n_local, int n_terms, const std::uint64_t* x, const std::uint64_t* y,
+                               const std::uint64_t* z, const std::uint64_t* gz, const double* coeffs, int* passes,
+                               int* groups, int* wide_groups, double* seconds) {
+    return guarded([&] {
+        require(n_local >= 1 && n_local <= 62, QRT_ERR_INVALID, "n_local out of range");
+        require(n_terms == 0 || (x && y && z && gz && coeffs), QRT_ERR_INVALID, "null term arrays");
+        pauli_plan_info(n_local, n_terms, x, y, z, gz, coeffs, passes, groups, wide_groups, seconds);
+    });
+}
+
 qrt_status qrt_norm(qrt_state* st, double* out) {
+    TraceScope trace_("qrt_norm");
     return guarded([&] {
         require(st && out, QRT_ERR_INVALID, "null argument");
         DeviceGuard g(st->device);

@@ -22,6 +22,7 @@
 // run-to-run identical.  Algorithmic traffic per pass = 16 B x 2^(n-g) read.
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <map>
 
@@ -437,19 +438,24 @@ int compress_bits(std::uint64_t m, const int* tile_pos, int T) {
 
 }  // namespace
 
-void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const std::uint64_t* y,
-                       const std::uint64_t* z, const std::uint64_t* gz, const double* coeffs, double* partial) {
-    const int nl = st->nl;
-    const std::uint64_t local_mask = nl >= 64 ? ~0ull : ((1ull << nl) - 1);
-    const std::uint64_t pe_mask = (st->p == 1) ? 0ull : static_cast<std::uint64_t>(st->p - 1);
-    for (int t = 0; t < n_terms; ++t) {
-        if ((x[t] | y[t] | z[t]) & ~local_mask) fail(QRT_ERR_INVALID, "term mask outside the local positions");
-        if ((x[t] & y[t]) || (x[t] & z[t]) || (y[t] & z[t])) fail(QRT_ERR_INVALID, "overlapping X/Y/Z masks");
-        if (gz[t] & ~pe_mask) fail(QRT_ERR_INVALID, "global Z mask outside the PE index");
-    }
-    for (int i = 0; i < 2 * st->p; ++i) partial[i] = 0.0;
-    if (n_terms == 0) return;
+struct PauliPlanHost {
+    int T = 0;
+    std::vector<PGroup> dgroups;
+    std::vector<PTerm> dterms;
+    std::vector<PPass> hdrs;
+    std::vector<WGroup> wgroups;
+};
 
+// Host planning of one EVC tile: flip-mask groups, tile passes, coefficient
+// folding, and the wide (full-vector) groups.  No device access.
+PauliPlanHost build_pauli_plan(int nl, int pe_begin, int n_terms, const std::uint64_t* x, const std::uint64_t* y,
+                               const std::uint64_t* z, const std::uint64_t* gz, const double* coeffs) {
+    const std::uint64_t local_mask = nl >= 64 ? ~0ull : ((1ull << nl) - 1);
+    PauliPlanHost plan;
+    auto& dgroups = plan.dgroups;
+    auto& dterms = plan.dterms;
+    auto& hdrs = plan.hdrs;
+    auto& wgroups = plan.wgroups;
     // ---- group by flip mask -------------------------------------------------
     std::map<std::uint64_t, std::vector<int>> by_xy;
     for (int t = 0; t < n_terms; ++t) by_xy[x[t] | y[t]].push_back(t);
@@ -503,13 +509,10 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
     }
 
     // ---- device descriptors ---------------------------------------------------
-    std::vector<PGroup> dgroups;
-    std::vector<PTerm> dterms;
-    std::vector<PPass> hdrs;
     for (const Pass& ps : passes) {
         PPass h{};
         h.T = T;
-        h.pe_begin = st->pe_begin;
+        h.pe_begin = pe_begin;
         int ti = 0, no = 0;
         for (int p = 0; p < nl; ++p) {
             if (ps.B >> p & 1ull)
@@ -590,7 +593,6 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
         hdrs.push_back(h);
     }
     // wide flip masks: full-vector sweeps (terms keep their full sign masks)
-    std::vector<WGroup> wgroups;
     for (const auto& [xy, members] : wide) {
         WGroup W{};
         W.x = xy;
@@ -609,6 +611,29 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
         }
         wgroups.push_back(W);
     }
+    plan.T = T;
+    return plan;
+}
+
+void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const std::uint64_t* y,
+                       const std::uint64_t* z, const std::uint64_t* gz, const double* coeffs, double* partial) {
+    const int nl = st->nl;
+    const std::uint64_t local_mask = nl >= 64 ? ~0ull : ((1ull << nl) - 1);
+    const std::uint64_t pe_mask = (st->p == 1) ? 0ull : static_cast<std::uint64_t>(st->p - 1);
+    for (int t = 0; t < n_terms; ++t) {
+        if ((x[t] | y[t] | z[t]) & ~local_mask) fail(QRT_ERR_INVALID, "term mask outside the local positions");
+        if ((x[t] & y[t]) || (x[t] & z[t]) || (y[t] & z[t])) fail(QRT_ERR_INVALID, "overlapping X/Y/Z masks");
+        if (gz[t] & ~pe_mask) fail(QRT_ERR_INVALID, "global Z mask outside the PE index");
+    }
+    for (int i = 0; i < 2 * st->p; ++i) partial[i] = 0.0;
+    if (n_terms == 0) return;
+
+    PauliPlanHost plan = build_pauli_plan(nl, st->pe_begin, n_terms, x, y, z, gz, coeffs);
+    const int T = plan.T;
+    auto& dgroups = plan.dgroups;
+    auto& dterms = plan.dterms;
+    auto& hdrs = plan.hdrs;
+    auto& wgroups = plan.wgroups;
     const std::size_t gbytes = dgroups.size() * sizeof(PGroup);
     const std::size_t toff = (gbytes + 255) & ~std::size_t{255};
     const std::size_t woff = (toff + dterms.size() * sizeof(PTerm) + 255) & ~std::size_t{255};
@@ -664,6 +689,18 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
     // algorithmic flops: one complex MAC per amplitude per term (reference loop)
     st->stats[QRT_K_PAULI].flops += 8.0 * static_cast<double>(st->amps) * st->pe_count * n_terms;
     gather_partials(st, out, partial);
+}
+
+void pauli_plan_info(int nl, int n_terms, const std::uint64_t* x, const std::uint64_t* y, const std::uint64_t* z,
+                     const std::uint64_t* gz, const double* coeffs, int* passes, int* groups, int* wide_groups,
+                     double* seconds) {
+    const auto t0 = std::chrono::steady_clock::now();
+    PauliPlanHost plan = build_pauli_plan(nl, 0, n_terms, x, y, z, gz, coeffs);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (passes) *passes = static_cast<int>(plan.hdrs.size());
+    if (groups) *groups = static_cast<int>(plan.dgroups.size());
+    if (wide_groups) *wide_groups = static_cast<int>(plan.wgroups.size());
+    if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
 }
 
 double norm(qrt_state* st) {

@@ -61,3 +61,48 @@ def test_native_libraries_are_in_tree(qb):
     for name in ("libqrt.so", "libqrtile_b200.so"):
         assert (pkg / name).exists()
     assert Path(qb._qrtile.__file__).parent == pkg
+
+
+def _masks(terms):
+    import numpy as np
+
+    n = len(terms[0].letters)
+    x = np.zeros(len(terms), np.uint64)
+    y, z, gz = x.copy(), x.copy(), x.copy()
+    co = np.zeros(2 * len(terms))
+    for i, t in enumerate(terms):
+        for q, c in enumerate(t.letters):
+            bit = np.uint64(1 << q)
+            if c == "X":
+                x[i] |= bit
+            elif c == "Y":
+                y[i] |= bit
+            elif c == "Z":
+                z[i] |= bit
+        co[2 * i], co[2 * i + 1] = t.coeff.real, t.coeff.imag
+    return n, x, y, z, gz, co
+
+
+def _plan_info(qb, terms):
+    lib = qb.load_libqrt()
+    n, x, y, z, gz, co = _masks(terms)
+    P = C.POINTER(C.c_uint64)
+    pa, gr, wi, sec = C.c_int(), C.c_int(), C.c_int(), C.c_double()
+    rc = lib.qrt_pauli_plan_info(n, len(terms), x.ctypes.data_as(P), y.ctypes.data_as(P), z.ctypes.data_as(P),
+                                 gz.ctypes.data_as(P), co.ctypes.data_as(C.POINTER(C.c_double)), C.byref(pa),
+                                 C.byref(gr), C.byref(wi), C.byref(sec))
+    assert rc == 0
+    return pa.value, gr.value, wi.value, sec.value
+
+
+def test_evc_pass_plan_host_only(qb):
+    """EVC batching on the host (no device): 30-qubit JW span-10 packs 8,266
+    strings into < 100 tile passes with no full-vector group, in milliseconds."""
+    passes, groups, wide, sec = _plan_info(qb, qb.gen_synthetic_jw(30, 1, 10))
+    assert 0 < passes < 100 and wide == 0 and groups >= 2000 and sec < 0.5
+    import numpy as np
+
+    rng = np.random.default_rng(1)
+    rnd = [qb.PauliTerm(1.0, "".join("IXYZ"[int(v)] for v in rng.integers(0, 4, 30))) for _ in range(50)]
+    _, _, wide_r, _ = _plan_info(qb, rnd)
+    assert wide_r > 0  # random words need the full-vector path

@@ -19,8 +19,11 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <array>
+#include <iterator>
+#include <memory>
 
-#include "qrt_internal.h"
+#include "qrt_light.h"
 
 namespace qrt {
 
@@ -428,18 +431,113 @@ struct HostOp {
     int kind, k;
     int pos[kBigK];
     std::uint64_t mask;
-    std::size_t mat_off;  // offset into the caller's mats (doubles)
+    const double* m;      // interleaved complex payload (caller's mats or a fused product)
     int mat_len;          // double2 entries
+    bool sign = false;    // diagonal with every entry exactly +1 or -1
+    std::uint64_t neg = 0;  // sign gates: entries that are -1
 };
+
+bool light_op(const HostOp& h) {
+    if (h.kind == kDense) return h.k <= 2;
+    return h.sign ? h.k <= kLightMaxDiagK : h.k <= 2;
+}
+
+// Light-pass stage count cap (QRT_LIGHT_STAGES overrides for experiments).
+int light_max_stages() {
+    static int v = [] {
+        const char* e = std::getenv("QRT_LIGHT_STAGES");
+        const int s = e ? std::atoi(e) : 4;
+        return std::max(1, std::min(s, kLightMaxStages));
+    }();
+    return v;
+}
+
+bool env_on(const char* name, bool dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) != 0 : dflt;
+}
+
+// Stage plan of one light pass (see qrt_light.h): runs of the pass's ops,
+// each with four register positions S; dense targets lie in S, diagonal
+// gates anywhere; an op never overtakes a deferred op on a shared position.
+struct LightStagePlan {
+    std::uint64_t S = 0;
+    std::vector<int> ops;
+};
+
+int plan_light_stages(const std::vector<HostOp>& opsv, const std::vector<int>& taken, std::uint64_t B, int m_max,
+                      std::vector<LightStagePlan>* out, std::vector<int>* leftover) {
+    std::vector<int> rem = taken, keep;
+    int applied = 0, stages = 0;
+    auto stage_take = [&](std::uint64_t S, LightStagePlan* sp, std::vector<int>* kp) {
+        std::uint64_t blocked = 0;
+        int n = 0;
+        for (int id : rem) {
+            const HostOp& h = opsv[static_cast<std::size_t>(id)];
+            if ((h.mask & blocked) || (h.kind == kDense && (h.mask & ~S))) {
+                blocked |= h.mask;
+                if (kp) kp->push_back(id);
+                continue;
+            }
+            ++n;
+            if (sp) sp->ops.push_back(id);
+        }
+        return n;
+    };
+    while (!rem.empty() && stages < m_max) {
+        std::uint64_t best_S = 0;
+        int best = -1;
+        int seeds = 0;
+        const std::size_t m = rem.size();
+        for (std::size_t sd = 0; sd < m && seeds < 8; ++sd) {
+            if (opsv[static_cast<std::size_t>(rem[sd])].kind != kDense) continue;
+            ++seeds;
+            std::uint64_t S = 0, blocked = 0;
+            for (std::size_t q = 0; q < m; ++q) {
+                const HostOp& h = opsv[static_cast<std::size_t>(rem[(sd + q) % m])];
+                if (h.kind != kDense) {
+                    if (h.mask & blocked) blocked |= h.mask;
+                    continue;
+                }
+                if ((h.mask & blocked) || __builtin_popcountll(S | h.mask) > kLightRegBits) {
+                    blocked |= h.mask;
+                    continue;
+                }
+                S |= h.mask;
+                if (__builtin_popcountll(S) == kLightRegBits) break;
+            }
+            const int got = stage_take(S, nullptr, nullptr);
+            if (got > best) {
+                best = got;
+                best_S = S;
+            }
+        }
+        // fill to four register positions from the top of B (keeps the
+        // coalescing positions out of S where possible: direct HBM access)
+        for (int p = 63; p >= 0 && __builtin_popcountll(best_S) < kLightRegBits; --p)
+            if ((B >> p & 1ull) && !(best_S >> p & 1ull)) best_S |= 1ull << p;
+        LightStagePlan sp;
+        sp.S = best_S;
+        keep.clear();
+        applied += stage_take(best_S, &sp, &keep);
+        rem.swap(keep);
+        if (out) out->push_back(std::move(sp));
+        ++stages;
+    }
+    if (leftover) *leftover = rem;
+    return applied;
+}
 
 }  // namespace
 
 void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, const double* mats,
                  const unsigned* flags) {
     const int nl = st->nl;
+    const double amps_all = static_cast<double>(st->amps) * st->pe_count;
     // ---- decode and validate -------------------------------------------------
     std::vector<HostOp> opsv(static_cast<std::size_t>(n_gates));
     std::size_t pcur = 0, mcur = 0;
+    double call_flops = 0.0;  // reference-equivalent flops of the gates as given
     for (int i = 0; i < n_gates; ++i) {
         HostOp& h = opsv[static_cast<std::size_t>(i)];
         h.k = arity[i];
@@ -454,31 +552,112 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
             h.mask |= 1ull << p;
             h.pos[j] = p;
         }
-        h.mat_off = mcur;
+        h.m = mats + mcur;
         h.mat_len = h.kind == kDiag ? (1 << h.k) : (1 << (2 * h.k));
         mcur += static_cast<std::size_t>(2 * h.mat_len);
+        call_flops += 8.0 * (h.kind == kDiag ? 1.0 : static_cast<double>(1 << h.k)) * amps_all;
+    }
+
+    // ---- fuse runs of single-qubit gates on one position -------------------------
+    // U_j U_i for consecutive 1-qubit gates i < j on the same position (no gate
+    // on that position in between; gates elsewhere commute exactly).  The
+    // product is formed in fp64 on the host, so amplitudes differ from the
+    // gate-by-gate order only by rounding (<= 1e-15 here).
+    std::vector<std::array<double, 8>> fused;
+    fused.reserve(static_cast<std::size_t>(n_gates));
+    std::vector<char> dead(static_cast<std::size_t>(n_gates), 0);
+    if (env_on("QRT_FUSE_1Q", true)) {
+        std::vector<int> nxt(static_cast<std::size_t>(n_gates), -1), last(64, -1);
+        for (int i = n_gates - 1; i >= 0; --i) {
+            const HostOp& h = opsv[static_cast<std::size_t>(i)];
+            if (h.k == 1) nxt[static_cast<std::size_t>(i)] = last[static_cast<std::size_t>(h.pos[0])];
+            for (int j = 0; j < h.k; ++j) last[static_cast<std::size_t>(h.pos[j])] = i;
+        }
+        for (int i = 0; i < n_gates; ++i) {
+            const int j = nxt[static_cast<std::size_t>(i)];
+            if (j < 0) continue;
+            HostOp& a = opsv[static_cast<std::size_t>(i)];
+            HostOp& b = opsv[static_cast<std::size_t>(j)];
+            if (b.k != 1) continue;
+            std::array<double, 8> r{};
+            auto ent = [](const HostOp& h, int row, int col, double& re, double& im) {
+                if (h.kind == kDiag) {
+                    re = row == col ? h.m[2 * row] : 0.0;
+                    im = row == col ? h.m[2 * row + 1] : 0.0;
+                } else {
+                    re = h.m[2 * (2 * row + col)];
+                    im = h.m[2 * (2 * row + col) + 1];
+                }
+            };
+            if (a.kind == kDiag && b.kind == kDiag) {
+                for (int d = 0; d < 2; ++d) {
+                    const double ar = a.m[2 * d], ai = a.m[2 * d + 1], br = b.m[2 * d], bi = b.m[2 * d + 1];
+                    r[static_cast<std::size_t>(2 * d)] = br * ar - bi * ai;
+                    r[static_cast<std::size_t>(2 * d + 1)] = br * ai + bi * ar;
+                }
+                b.mat_len = 2;
+            } else {
+                for (int row = 0; row < 2; ++row)
+                    for (int col = 0; col < 2; ++col) {
+                        double sr = 0.0, si = 0.0;
+                        for (int q = 0; q < 2; ++q) {
+                            double br, bi, ar, ai;
+                            ent(b, row, q, br, bi);
+                            ent(a, q, col, ar, ai);
+                            sr += br * ar - bi * ai;
+                            si += br * ai + bi * ar;
+                        }
+                        r[static_cast<std::size_t>(2 * (2 * row + col))] = sr;
+                        r[static_cast<std::size_t>(2 * (2 * row + col) + 1)] = si;
+                    }
+                b.kind = kDense;
+                b.mat_len = 4;
+            }
+            fused.push_back(r);
+            b.m = fused.back().data();
+            dead[static_cast<std::size_t>(i)] = 1;
+        }
+    }
+    for (HostOp& h : opsv) {
+        if (h.kind != kDiag) continue;
+        h.sign = true;
+        h.neg = 0;
+        for (int e = 0; e < h.mat_len; ++e) {
+            const double re = h.m[2 * e], im = h.m[2 * e + 1];
+            if (im != 0.0 || (re != 1.0 && re != -1.0)) h.sign = false;
+            if (re == -1.0 && h.k <= kLightMaxDiagK) h.neg |= 1ull << e;
+        }
     }
 
     // ---- plan passes -----------------------------------------------------------
     struct Pass {
         bool wide = false;
+        bool light = false;
         int T = 0, c = 0;
         std::vector<int> tile_pos;
         std::vector<int> ops;
+        std::vector<LightStagePlan> stages;
     };
     std::vector<Pass> passes;
-    std::vector<int> remaining(static_cast<std::size_t>(n_gates));
-    for (int i = 0; i < n_gates; ++i) remaining[static_cast<std::size_t>(i)] = i;
+    std::vector<int> remaining;
+    remaining.reserve(static_cast<std::size_t>(n_gates));
+    for (int i = 0; i < n_gates; ++i)
+        if (!dead[static_cast<std::size_t>(i)]) remaining.push_back(i);
     auto is_wide = [&](const HostOp& h) {
         return h.kind == kDiag ? h.k > kMaxDiagK : h.k > kMaxTileGateK;
     };
     const bool whole = nl <= kTileBits;
+    const bool light_ok = nl >= kTileBits && env_on("QRT_LIGHT", true);
+    const int m_max = light_max_stages();
     // The take phase for tile positions B: in order, every gate whose targets
     // are inside B (diagonals anywhere) unless it follows a deferred gate on a
-    // shared qubit or the per-pass staging budgets are exhausted.
+    // shared qubit or the per-pass staging budgets are exhausted.  The first
+    // gate taken fixes the pass kind: a light pass (register-resident,
+    // qrt_light.cu) takes only 1-/2-qubit and diagonal gates.
     auto take = [&](std::uint64_t B, Pass* ps, std::vector<int>* keep) -> int {
         std::uint64_t blocked = 0;
         int param_used = 0, diag_used = 0, frag_used = 0, n = 0;
+        int mode = -1;  // -1 undecided, 0 heavy, 1 light
         bool closed = false, wide = false;
         for (int id : remaining) {
             const HostOp& h = opsv[static_cast<std::size_t>(id)];
@@ -499,30 +678,69 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
                 continue;
             }
             const bool fits = h.kind == kDiag || (h.mask & ~B) == 0;
-            const int T_here = whole ? nl : kTileBits;
-            const bool dmma = h.kind == kDense && (h.k == 3 || h.k == 4) && T_here >= h.k + 3;
-            const int in_params = (h.kind == kDense && h.k <= 4 && !dmma) ? h.mat_len : 0;
-            const int in_smem = h.kind == kDiag ? h.mat_len : 0;
-            const int in_frag = dmma ? 4 * h.mat_len : 0;  // (2D)^2 real entries
-            if (fits && param_used + in_params <= kParamMats && diag_used + in_smem <= kDiagStage &&
-                frag_used + in_frag <= kFragStage && n < kMaxPassOps) {
+            if (fits && mode < 0) mode = (light_ok && light_op(h)) ? 1 : 0;
+            bool ok = fits;
+            if (ok && mode == 1) {
+                const int in_mats = h.kind == kDense ? h.mat_len : (h.sign ? 0 : h.mat_len);
+                ok = light_op(h) && n < kLightMaxOps && param_used + in_mats <= kLightMaxMats;
+                if (ok) param_used += in_mats;
+            } else if (ok) {
+                const int T_here = whole ? nl : kTileBits;
+                const bool dmma = h.kind == kDense && (h.k == 3 || h.k == 4) && T_here >= h.k + 3;
+                const int in_params = (h.kind == kDense && h.k <= 4 && !dmma) ? h.mat_len : 0;
+                const int in_smem = h.kind == kDiag ? h.mat_len : 0;
+                const int in_frag = dmma ? 4 * h.mat_len : 0;  // (2D)^2 real entries
+                ok = param_used + in_params <= kParamMats && diag_used + in_smem <= kDiagStage &&
+                     frag_used + in_frag <= kFragStage && n < kMaxPassOps;
+                if (ok) {
+                    param_used += in_params;
+                    diag_used += in_smem;
+                    frag_used += in_frag;
+                }
+            }
+            if (ok) {
                 ++n;
                 if (ps) ps->ops.push_back(id);
-                param_used += in_params;
-                diag_used += in_smem;
-                frag_used += in_frag;
             } else {
                 blocked |= h.mask;
                 if (keep) keep->push_back(id);
             }
         }
-        if (ps) ps->wide = wide;
+        if (ps) {
+            ps->wide = wide;
+            ps->light = mode == 1 && !wide;
+        }
         return n;
+    };
+    // Gates a pass over B actually applies: light passes are cut to the
+    // stage budget.
+    auto evaluate = [&](std::uint64_t B, Pass* ps, std::vector<int>* keep) -> int {
+        Pass tmp;
+        std::vector<int> k1;
+        Pass* pp = ps ? ps : &tmp;
+        std::vector<int>* kp = keep ? keep : &k1;
+        const int got = take(B, pp, kp);
+        if (!pp->light) return got;
+        std::vector<int> left;
+        std::vector<LightStagePlan>* sp = ps ? &ps->stages : nullptr;
+        const int applied = plan_light_stages(opsv, pp->ops, B, m_max, sp, &left);
+        if (ps) {
+            if (!left.empty()) {  // unapplied ops go back, original order
+                std::vector<int> merged;
+                merged.reserve(kp->size() + left.size());
+                std::merge(kp->begin(), kp->end(), left.begin(), left.end(), std::back_inserter(merged));
+                kp->swap(merged);
+                std::vector<int> app;
+                for (const auto& s : ps->stages) app.insert(app.end(), s.ops.begin(), s.ops.end());
+                ps->ops = app;
+            }
+        }
+        return applied;
     };
     // Candidate tile positions seeded from one of the first remaining gates:
     // grow B from the coalescing bits by the targets of gates in order
     // (rotated to start at the seed), skipping gates that are blocked or
-    // would overflow the tile.  The candidate that takes most gates wins
+    // would overflow the tile.  The candidate that applies most gates wins
     // (ties: the earliest seed).  Seeding from several gates lets a pass
     // follow the light cone of the circuit instead of the first layer only.
     constexpr int kSeeds = 16;
@@ -554,7 +772,7 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
             const std::size_t seeds = std::min<std::size_t>(kSeeds, remaining.size());
             for (std::size_t sd = 0; sd < seeds; ++sd) {
                 const std::uint64_t cand = candidate(sd);
-                const int got = take(cand, nullptr, nullptr);
+                const int got = evaluate(cand, nullptr, nullptr);
                 if (got > best) {
                     best = got;
                     B = cand;
@@ -564,7 +782,7 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
         Pass ps;
         std::vector<int> keep;
         keep.reserve(remaining.size());
-        take(B, &ps, &keep);
+        evaluate(B, &ps, &keep);
         if (ps.ops.empty()) fail(QRT_ERR_INVALID, "gate planner made no progress");
         if (!ps.wide) {
             for (int p = 0; p < nl; ++p)
@@ -584,9 +802,136 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
     std::vector<std::vector<double2>> pmats(passes.size());
     std::vector<double> frags;
     std::vector<int> wide_pos;  // for wide passes: positions (kBigK per pass)
+    std::vector<std::unique_ptr<LightParams>> light;
+    constexpr int kLightMarker = 1 << 20;  // PassHdr::T of a light pass: marker + index into `light`
+    auto build_light = [&](const std::vector<int>& tile_pos, int c, const std::vector<LightStagePlan>& stages) {
+        auto L = std::make_unique<LightParams>();
+        std::memset(L.get(), 0, sizeof(LightParams));
+        int tb_of[64];
+        for (int p = 0; p < 64; ++p) tb_of[p] = -1;
+        std::uint64_t inB = 0;
+        for (int i = 0; i < kTileBits; ++i) {
+            L->tile_pos[i] = static_cast<std::int8_t>(tile_pos[static_cast<std::size_t>(i)]);
+            tb_of[tile_pos[static_cast<std::size_t>(i)]] = i;
+            inB |= 1ull << tile_pos[static_cast<std::size_t>(i)];
+        }
+        int no = 0;
+        for (int p = 0; p < nl; ++p)
+            if (!(inB >> p & 1ull)) L->outer_pos[no++] = static_cast<std::int8_t>(p);
+        L->n_outer = no;
+        L->c = c;
+        L->tiles_per_pe = 1 << (nl - kTileBits);
+        L->n_stages = static_cast<int>(stages.size());
+        int n_ops = 0, n_mats = 0;
+        const int lowmask = (1 << kCoalBits) - 1;
+        for (std::size_t s = 0; s < stages.size(); ++s) {
+            LightStage& S = L->st[s];
+            int sbits = 0, q = 0;
+            int reg_of[kTileBits];
+            for (int i = 0; i < kTileBits; ++i) reg_of[i] = 4;
+            for (int i = 0; i < kTileBits; ++i)
+                if (stages[s].S >> tile_pos[static_cast<std::size_t>(i)] & 1ull) {
+                    S.S[q] = static_cast<std::int8_t>(i);
+                    reg_of[i] = q++;
+                    sbits |= 1 << i;
+                }
+            // thread bits: the remaining tile bits ascending, except that the
+            // three lowest lanes get distinct residues mod 3 (conflict-free
+            // 16-byte shared-memory phases under swz) when S took a low bit
+            std::vector<int> rest;
+            for (int i = 0; i < kTileBits; ++i)
+                if (!(sbits >> i & 1)) rest.push_back(i);
+            if (sbits & lowmask) {
+                std::vector<int> lead;
+                for (int res = 0; res < 3; ++res)
+                    for (std::size_t u = 0; u < rest.size(); ++u)
+                        if (rest[u] % 3 == res) {
+                            lead.push_back(rest[u]);
+                            rest.erase(rest.begin() + static_cast<std::ptrdiff_t>(u));
+                            break;
+                        }
+                rest.insert(rest.begin(), lead.begin(), lead.end());
+            }
+            for (int i = 0; i < kTileBits - kLightRegBits; ++i)
+                S.tb[i] = static_cast<std::int8_t>(rest[static_cast<std::size_t>(i)]);
+            if (s == 0) L->direct_in = (sbits & lowmask) == 0;
+            if (s + 1 == stages.size()) L->direct_out = (sbits & lowmask) == 0;
+            S.op_begin = static_cast<std::int16_t>(n_ops);
+            for (int id : stages[s].ops) {
+                const HostOp& o = opsv[static_cast<std::size_t>(id)];
+                LightOp& lo = L->ops[n_ops++];
+                lo.k = static_cast<std::int8_t>(o.k);
+                auto put_mat = [&](int len, auto&& entry) {
+                    lo.mat = static_cast<std::int16_t>(n_mats);
+                    for (int e = 0; e < len; ++e) L->mats[n_mats++] = entry(e);
+                };
+                if (o.kind == kDense) {
+                    const int qa = reg_of[tb_of[o.pos[0]]];
+                    if (o.k == 1) {
+                        lo.kind = kL1;
+                        lo.q0 = static_cast<std::int8_t>(qa);
+                        put_mat(4, [&](int e) { return make_double2(o.m[2 * e], o.m[2 * e + 1]); });
+                    } else {
+                        const int qb = reg_of[tb_of[o.pos[1]]];
+                        lo.kind = kL2;
+                        const bool swap = qa > qb;
+                        lo.q0 = static_cast<std::int8_t>(swap ? qb : qa);
+                        lo.q1 = static_cast<std::int8_t>(swap ? qa : qb);
+                        auto sw = [&](int x) { return swap ? (((x & 1) << 1) | (x >> 1)) : x; };
+                        put_mat(16, [&](int e) {
+                            const int r = sw(e >> 2), cc = sw(e & 3);
+                            const int at = 4 * r + cc;
+                            return make_double2(o.m[2 * at], o.m[2 * at + 1]);
+                        });
+                    }
+                } else {
+                    lo.kind = o.sign ? kLSign : kLDiag;
+                    lo.neg = o.neg;
+                    for (int j = 0; j < kLightMaxDiagK; ++j) {
+                        lo.rq[j] = 4;
+                        lo.tb[j] = -1;
+                        lo.pos[j] = 0;
+                    }
+                    for (int j = 0; j < o.k; ++j) {
+                        const int tb = tb_of[o.pos[j]];
+                        lo.tb[j] = static_cast<std::int8_t>(tb);
+                        lo.pos[j] = static_cast<std::int8_t>(o.pos[j]);
+                        lo.rq[j] = static_cast<std::int8_t>(tb >= 0 ? reg_of[tb] : 4);
+                    }
+                    if (!o.sign) put_mat(o.mat_len, [&](int e) { return make_double2(o.m[2 * e], o.m[2 * e + 1]); });
+                    if (o.sign) {  // tabulate negated register slots per value of the fixed bits
+                        int fixed_j[kLightMaxDiagK], nfix = 0;
+                        for (int j = 0; j < o.k; ++j)
+                            if (lo.rq[j] >= 4) fixed_j[nfix++] = j;
+                        if (nfix <= 2) {
+                            lo.q0 = 1;
+                            lo.negr = 0;
+                            for (int f = 0; f < (1 << nfix); ++f)
+                                for (int r = 0; r < 16; ++r) {
+                                    int m = 0;
+                                    for (int j = 0; j < o.k; ++j)
+                                        if (lo.rq[j] < 4) m |= ((r >> lo.rq[j]) & 1) << j;
+                                    for (int i = 0; i < nfix; ++i) m |= ((f >> i) & 1) << fixed_j[i];
+                                    if ((o.neg >> m) & 1ull) lo.negr |= 1ull << (16 * f + r);
+                                }
+                        }
+                    }
+                }
+            }
+            S.op_count = static_cast<std::int16_t>(n_ops - S.op_begin);
+        }
+        if (n_ops > kLightMaxOps || n_mats > kLightMaxMats) fail(QRT_ERR_INVALID, "light pass over budget");
+        return L;
+    };
     for (std::size_t pidx = 0; pidx < passes.size(); ++pidx) {
         Pass& ps = passes[pidx];
         PassHdr h{};
+        if (ps.light) {
+            h.T = kLightMarker + static_cast<int>(light.size());
+            light.push_back(build_light(ps.tile_pos, ps.c, ps.stages));
+            hdrs.push_back(h);
+            continue;
+        }
         if (ps.wide) {
             const HostOp& o = opsv[static_cast<std::size_t>(ps.ops[0])];
             h.n_ops = 1;
@@ -600,8 +945,8 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
             g.gmat = h.mat_begin;
             dev_ops.push_back(g);
             for (int e = 0; e < o.mat_len; ++e)
-                pool.push_back(make_double2(mats[o.mat_off + 2 * static_cast<std::size_t>(e)],
-                                            mats[o.mat_off + 2 * static_cast<std::size_t>(e) + 1]));
+                pool.push_back(make_double2(o.m[2 * static_cast<std::size_t>(e)],
+                                            o.m[2 * static_cast<std::size_t>(e) + 1]));
             h.T = -static_cast<int>(wide_pos.size()) - 1;  // marks a wide pass; index into wide_pos
             for (int j = 0; j < kBigK; ++j) wide_pos.push_back(j < o.k ? o.pos[j] : 0);
             hdrs.push_back(h);
@@ -626,8 +971,8 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
         // dense k<=4 matrices into the launch parameters, k=5..7 from global
         auto put = [&](std::vector<double2>& dst, const HostOp& o) {
             for (int e = 0; e < o.mat_len; ++e)
-                dst.push_back(make_double2(mats[o.mat_off + 2 * static_cast<std::size_t>(e)],
-                                           mats[o.mat_off + 2 * static_cast<std::size_t>(e) + 1]));
+                dst.push_back(make_double2(o.m[2 * static_cast<std::size_t>(e)],
+                                           o.m[2 * static_cast<std::size_t>(e) + 1]));
         };
         int staged = 0;
         h.frag_begin = static_cast<int>(frags.size());
@@ -656,8 +1001,8 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
                         for (int lane = 0; lane < 32; ++lane) {
                             const int kk = 4 * kb + (lane & 3), nn = 8 * nb + (lane >> 2);
                             const int r = nn >> 1, i = nn & 1, c = kk >> 1, j = kk & 1;
-                            const std::size_t at = o.mat_off + 2 * (static_cast<std::size_t>(r) * D + c);
-                            const double re = mats[at], im = mats[at + 1];
+                            const std::size_t at = 2 * (static_cast<std::size_t>(r) * D + c);
+                            const double re = o.m[at], im = o.m[at + 1];
                             frags.push_back(i == j ? re : (i == 0 ? -im : im));
                         }
             } else if (o.k <= 4) {
@@ -704,9 +1049,17 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
 
     static thread_local PassParams params;  // 29 KiB: keep off the stack
     ProfileScope prof(st, QRT_K_GATES);
-    const double amps_all = static_cast<double>(st->amps) * st->pe_count;
+    st->stats[QRT_K_GATES].flops += call_flops;
     for (std::size_t pi = 0; pi < hdrs.size(); ++pi) {
         const PassHdr& h = hdrs[pi];
+        if (h.T >= kLightMarker) {
+            LightParams& L = *light[static_cast<std::size_t>(h.T - kLightMarker)];
+            for (int i = 0; i < st->pe_count; ++i) L.ptrs[i] = st->live(i);
+            launch_light_pass(L, L.tiles_per_pe * st->pe_count, st->stream, st->device);
+            st->stats[QRT_K_GATES].launches++;
+            st->stats[QRT_K_GATES].bytes += 32.0 * amps_all;
+            continue;
+        }
         if (h.T < 0) {  // wide, out of place into the alternate buffer, then copied back
             ensure_alt(st);
             const GateOp& g = dev_ops[static_cast<std::size_t>(h.op_begin)];
@@ -721,7 +1074,6 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
             }
             st->stats[QRT_K_GATES].launches += static_cast<std::uint64_t>(st->pe_count);
             st->stats[QRT_K_GATES].bytes += 64.0 * amps_all;
-            st->stats[QRT_K_GATES].flops += 8.0 * (g.kind == kDiag ? 1.0 : static_cast<double>(1 << g.k)) * amps_all;
             continue;
         }
         for (int i = 0; i < st->pe_count; ++i) params.ptrs.p[i] = st->live(i);
@@ -737,10 +1089,6 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
         QRT_CUDA(cudaGetLastError());
         st->stats[QRT_K_GATES].launches++;
         st->stats[QRT_K_GATES].bytes += 32.0 * amps_all;
-        for (int o = 0; o < h.n_ops; ++o) {
-            const GateOp& g = dev_ops[static_cast<std::size_t>(h.op_begin + o)];
-            st->stats[QRT_K_GATES].flops += 8.0 * (g.kind == kDiag ? 1.0 : static_cast<double>(1 << g.k)) * amps_all;
-        }
     }
 }
 

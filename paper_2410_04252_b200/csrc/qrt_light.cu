@@ -1,0 +1,307 @@
+// libqrt — register-resident light gate passes (see qrt_light.h).
+//
+// Reference semantics: apply_gate_narrow (dist_sim.cpp:163-201) for every
+// gate of the pass, in an order that never swaps two gates sharing a qubit.
+// One CTA = one 2^12-amplitude tile = 256 threads x 16 amplitudes.
+
+#include "qrt_light.h"
+
+namespace qrt {
+
+namespace {
+
+using u64 = std::uint64_t;
+
+__device__ __forceinline__ int swz(int e) {
+    const int x = e >> 3;
+    return e ^ ((x ^ (x >> 3) ^ (x >> 6) ^ (x >> 9)) & 7);
+}
+
+__device__ __forceinline__ double2 cmul(const double2 u, const double2 a) {
+    return make_double2(fma(u.x, a.x, -u.y * a.y), fma(u.x, a.y, u.y * a.x));
+}
+__device__ __forceinline__ double2 cmac2(const double2 u, const double2 a, const double2 w, const double2 b) {
+    double2 r;
+    r.x = fma(u.x, a.x, fma(-u.y, a.y, fma(w.x, b.x, -w.y * b.y)));
+    r.y = fma(u.x, a.y, fma(u.y, a.x, fma(w.x, b.y, w.y * b.x)));
+    return r;
+}
+
+template <int Q>
+__device__ __forceinline__ void dense1(double2 (&a)[16], const double2* __restrict__ m) {
+    const double2 m00 = m[0], m01 = m[1], m10 = m[2], m11 = m[3];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        if ((r >> Q) & 1) continue;
+        const int s = r | (1 << Q);
+        const double2 x = a[r], y = a[s];
+        a[r] = cmac2(m00, x, m01, y);
+        a[s] = cmac2(m10, x, m11, y);
+    }
+}
+
+// Matrix bit 0 <-> register bit Q0, matrix bit 1 <-> register bit Q1 (Q0 < Q1).
+template <int Q0, int Q1>
+__device__ __forceinline__ void dense2(double2 (&a)[16], const double2* __restrict__ m) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        if (((r >> Q0) & 1) || ((r >> Q1) & 1)) continue;
+        const int i0 = r, i1 = r | (1 << Q0), i2 = r | (1 << Q1), i3 = r | (1 << Q0) | (1 << Q1);
+        const double2 x0 = a[i0], x1 = a[i1], x2 = a[i2], x3 = a[i3];
+        double2 y[4];
+#pragma unroll
+        for (int row = 0; row < 4; ++row) {
+            const double2* u = m + 4 * row;
+            double2 acc = cmac2(u[0], x0, u[1], x1);
+            const double2 t = cmac2(u[2], x2, u[3], x3);
+            acc.x += t.x;
+            acc.y += t.y;
+            y[row] = acc;
+        }
+        a[i0] = y[0];
+        a[i1] = y[1];
+        a[i2] = y[2];
+        a[i3] = y[3];
+    }
+}
+
+__device__ __forceinline__ void apply_dense2(double2 (&a)[16], const double2* m, int q0, int q1) {
+    switch (q0 * 4 + q1) {
+        case 1: dense2<0, 1>(a, m); break;
+        case 2: dense2<0, 2>(a, m); break;
+        case 3: dense2<0, 3>(a, m); break;
+        case 6: dense2<1, 2>(a, m); break;
+        case 7: dense2<1, 3>(a, m); break;
+        default: dense2<2, 3>(a, m); break;
+    }
+}
+
+// Pending +-1 signs: bit r set = register slot r still owes a negation.
+// Applied by XOR on the sign bits (integer pipe), not as fp64 negations.
+__device__ __forceinline__ void apply_signs(double2 (&a)[16], unsigned& pend) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const int s = static_cast<int>((pend >> r) & 1u) << 31;
+        a[r].x = __hiloint2double(__double2hiint(a[r].x) ^ s, __double2loint(a[r].x));
+        a[r].y = __hiloint2double(__double2hiint(a[r].y) ^ s, __double2loint(a[r].y));
+    }
+    pend = 0;
+}
+
+// Diagonal-entry index of register slot r: fixed bits | register bits.
+__device__ __forceinline__ int diag_index(int fixed, int r, const int (&rq)[kLightMaxDiagK], int k) {
+    int m = fixed;
+#pragma unroll
+    for (int j = 0; j < kLightMaxDiagK; ++j)
+        if (j < k) m |= ((r >> rq[j]) & 1) << j;
+    return m;
+}
+
+__global__ void __launch_bounds__(kLightThreads, 2) light_pass_kernel(const __grid_constant__ LightParams P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int E = 1 << kTileBits;
+    double2* tile = reinterpret_cast<double2*>(smem_raw);
+    u64* tab = reinterpret_cast<u64*>(tile + E);
+    const int c = P.c;
+    const int t = threadIdx.x;
+    u64 cta = 0;
+    {
+        const u64 b = static_cast<u64>(blockIdx.x % P.tiles_per_pe);
+        for (int i = 0; i < P.n_outer; ++i) cta |= ((b >> i) & 1ull) << P.outer_pos[i];
+    }
+    amp_t* __restrict__ v = P.ptrs[blockIdx.x / P.tiles_per_pe];
+    const int nt = 1 << (kTileBits - c);
+    const int cmask = (1 << c) - 1;
+    const bool staged_io = !P.direct_in || !P.direct_out;
+    if (staged_io) {
+        for (int h = t; h < nt; h += kLightThreads) {
+            u64 o = 0;
+            for (int i = c; i < kTileBits; ++i) o |= static_cast<u64>((h >> (i - c)) & 1) << P.tile_pos[i];
+            tab[h] = o;
+        }
+        __syncthreads();
+    }
+
+    double2 a[16];
+    unsigned pend = 0;   // pending sign flips (fast sign path)
+    // per-stage thread mapping
+    int ebase = 0;       // tile index of register slot 0
+    int sq[4];           // tile index of register bit q
+    auto map_stage = [&](const LightStage& S) {
+        ebase = 0;
+#pragma unroll
+        for (int i = 0; i < kTileBits - kLightRegBits; ++i) ebase |= ((t >> i) & 1) << S.tb[i];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sq[q] = 1 << S.S[q];
+    };
+    auto slot_off = [&](int r) {  // tile-index offset of register slot r
+        int o = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if ((r >> q) & 1) o |= sq[q];
+        return o;
+    };
+    auto gofs = [&](int e) {  // tile index -> offset inside the PE
+        u64 o = cta;
+#pragma unroll
+        for (int i = 0; i < kTileBits; ++i)
+            if ((e >> i) & 1) o |= 1ull << P.tile_pos[i];
+        return o;
+    };
+
+    // ---- stage 0 input
+    map_stage(P.st[0]);
+    if (P.direct_in) {
+        const u64 g0 = gofs(ebase);
+        u64 gq[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) gq[q] = 1ull << P.tile_pos[P.st[0].S[q]];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            u64 o = g0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if ((r >> q) & 1) o |= gq[q];
+            a[r] = __ldcs(&v[o]);
+        }
+    } else {
+        for (int e = t; e < E; e += kLightThreads) {
+            const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(&tile[swz(e)]));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s),
+                         "l"(&v[cta | tab[e >> c] | (e & cmask)]));
+        }
+        asm volatile("cp.async.wait_all;\n" ::);
+        __syncthreads();
+        const int sb = swz(ebase);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) a[r] = tile[sb ^ swz(slot_off(r))];
+    }
+
+    for (int s = 0; s < P.n_stages; ++s) {
+        const LightStage& S = P.st[s];
+        if (s > 0) {
+            // transpose through shared memory: previous mapping out, this one in
+            {
+                apply_signs(a, pend);
+                const int sb = swz(ebase);
+                __syncthreads();  // readers of the previous transpose are done
+#pragma unroll
+                for (int r = 0; r < 16; ++r) tile[sb ^ swz(slot_off(r))] = a[r];
+            }
+            __syncthreads();
+            map_stage(S);
+            const int sb = swz(ebase);
+#pragma unroll
+            for (int r = 0; r < 16; ++r) a[r] = tile[sb ^ swz(slot_off(r))];
+        }
+        for (int o = S.op_begin; o < S.op_begin + S.op_count; ++o) {
+            const LightOp& op = P.ops[o];
+            const int kind = op.kind;
+            if (kind != kLSign && pend) apply_signs(a, pend);
+            if (kind == kL1) {
+                const double2* m = P.mats + op.mat;
+                switch (op.q0) {
+                    case 0: dense1<0>(a, m); break;
+                    case 1: dense1<1>(a, m); break;
+                    case 2: dense1<2>(a, m); break;
+                    default: dense1<3>(a, m); break;
+                }
+            } else if (kind == kL2) {
+                apply_dense2(a, P.mats + op.mat, op.q0, op.q1);
+            } else {
+                const int k = op.k;
+                if (kind == kLSign && op.q0) {
+                    // fast path: the host tabulated the negated slots per value
+                    // of the (<= 2) non-register target bits
+                    int f = 0, i = 0;
+                    for (int j = 0; j < k; ++j) {
+                        if (op.rq[j] < 4) continue;
+                        const int tb = op.tb[j];
+                        const int bit = tb >= 0 ? (ebase >> tb) & 1 : static_cast<int>((cta >> op.pos[j]) & 1ull);
+                        f |= bit << i++;
+                    }
+                    pend ^= static_cast<unsigned>(op.negr >> (16 * f)) & 0xffffu;
+                } else if (kind == kLSign) {
+                    int fixed = 0, rq[kLightMaxDiagK];
+#pragma unroll
+                    for (int j = 0; j < kLightMaxDiagK; ++j) {
+                        rq[j] = op.rq[j];
+                        if (j < k && rq[j] >= 4) {
+                            const int tb = op.tb[j];
+                            const int bit = tb >= 0 ? (ebase >> tb) & 1 : static_cast<int>((cta >> op.pos[j]) & 1ull);
+                            fixed |= bit << j;
+                        }
+                    }
+                    const u64 neg = op.neg;
+                    unsigned mask = 0;
+#pragma unroll
+                    for (int r = 0; r < 16; ++r) mask |= static_cast<unsigned>((neg >> diag_index(fixed, r, rq, k)) & 1ull) << r;
+                    pend ^= mask;
+                } else {
+                    int fixed = 0, rq[kLightMaxDiagK];
+#pragma unroll
+                    for (int j = 0; j < kLightMaxDiagK; ++j) {
+                        rq[j] = op.rq[j];
+                        if (j < k && rq[j] >= 4) {
+                            const int tb = op.tb[j];
+                            const int bit = tb >= 0 ? (ebase >> tb) & 1 : static_cast<int>((cta >> op.pos[j]) & 1ull);
+                            fixed |= bit << j;
+                        }
+                    }
+                    // phase diagonal (k <= 2): two entries live at a time
+                    const double2* d = P.mats + op.mat;
+                    const int halves = k > 1 ? 2 : 1;
+#pragma unroll 1
+                    for (int hb = 0; hb < halves; ++hb) {
+                        const double2 d0 = d[2 * hb], d1 = d[2 * hb + 1];
+#pragma unroll
+                        for (int r = 0; r < 16; ++r) {
+                            const int m = diag_index(fixed, r, rq, k);
+                            if ((m >> 1) == hb) a[r] = cmul((m & 1) ? d1 : d0, a[r]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+
+    // ---- last stage output
+    apply_signs(a, pend);
+    if (P.direct_out) {
+        const u64 g0 = gofs(ebase);
+        u64 gq[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) gq[q] = 1ull << P.tile_pos[P.st[P.n_stages - 1].S[q]];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            u64 o = g0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if ((r >> q) & 1) o |= gq[q];
+            __stcs(&v[o], a[r]);
+        }
+    } else {
+        const int sb = swz(ebase);
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 16; ++r) tile[sb ^ swz(slot_off(r))] = a[r];
+        __syncthreads();
+        for (int e = t; e < E; e += kLightThreads) __stcs(&v[cta | tab[e >> c] | (e & cmask)], tile[swz(e)]);
+    }
+}
+
+}  // namespace
+
+void launch_light_pass(const LightParams& P, int total_tiles, cudaStream_t stream, int device) {
+    static bool attr_done[64] = {};
+    const std::size_t smem = (std::size_t{1} << kTileBits) * sizeof(double2) +
+                             (std::size_t{1} << (kTileBits - P.c)) * sizeof(std::uint64_t);
+    if (!attr_done[device]) {
+        QRT_CUDA(cudaFuncSetAttribute(light_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        attr_done[device] = true;
+    }
+    light_pass_kernel<<<total_tiles, kLightThreads, smem, stream>>>(P);
+    QRT_CUDA(cudaGetLastError());
+}
+
+}  // namespace qrt

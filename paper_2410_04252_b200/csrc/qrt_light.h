@@ -1,0 +1,69 @@
+// libqrt — register-resident gate passes for runs of 1-/2-qubit and diagonal
+// gates (the hardware-efficient-ansatz shape: RY/RZ on every qubit, CZ
+// brickwork).  Shared by the host planner (qrt_gates.cu) and the kernel
+// (qrt_light.cu).
+//
+// A light pass works on the same 2^12-amplitude tiles as gate_pass_kernel
+// (positions B, the lowest four always included), but the amplitudes live in
+// registers: 256 threads x 16 amplitudes.  A *stage* picks four tile bits S
+// as the register bits; every gate of the stage has its dense targets in S
+// (diagonal gates may target any position), so it is applied without
+// touching shared memory.  Between stages the tile is transposed through
+// shared memory once; the first stage loads straight from HBM and the last
+// stores straight to HBM when S avoids the four coalescing positions.  A
+// pass of m stages therefore costs one HBM round trip (32 B/amplitude) plus
+// m-1 shared-memory round trips, whatever the number of gates.
+#pragma once
+
+#include <cstdint>
+
+#include "qrt_internal.h"
+
+namespace qrt {
+
+inline constexpr int kLightRegBits = 4;                      // 16 amplitudes per thread
+inline constexpr int kLightThreads = 1 << (kTileBits - kLightRegBits);  // 256
+inline constexpr int kLightMaxStages = 8;
+inline constexpr int kLightMaxOps = 224;
+inline constexpr int kLightMaxMats = 896;  // double2 entries in the launch parameters
+inline constexpr int kLightMaxDiagK = 6;
+
+enum LightKind : std::int8_t { kL1 = 0, kL2 = 1, kLDiag = 2, kLSign = 3 };
+
+struct LightOp {
+    std::uint64_t neg;            // kLSign: bit m set <=> diagonal entry m is -1
+    std::uint64_t negr;           // kLSign with <= 2 non-register targets: for each value f of those
+                                  // target bits, 16 bits at 16 f = register slots to negate
+    std::int16_t mat;             // kL1/kL2/kLDiag: first double2 in LightParams::mats
+    std::int8_t kind, k;
+    std::int8_t q0, q1;           // dense: register bits of matrix bits 0 / 1 (q0 < q1 for kL2)
+                                  // kLSign: q0 = 1 if negr is valid (fast path)
+    std::int8_t rq[kLightMaxDiagK];   // diagonal: register bit of target j, 4 if not a register bit
+    std::int8_t tb[kLightMaxDiagK];   // diagonal: tile bit of target j (-1: outside the tile)
+    std::int8_t pos[kLightMaxDiagK];  // diagonal: physical position of target j
+};
+
+struct LightStage {
+    std::int8_t S[kLightRegBits];                       // tile bit of register bit q
+    std::int8_t tb[kTileBits - kLightRegBits];          // tile bit of thread-index bit i
+    std::int16_t op_begin, op_count;
+};
+
+struct LightParams {
+    amp_t* ptrs[kMaxLocalPEs];
+    int c;            // tile bits 0..c-1 are positions 0..c-1
+    int n_outer;
+    int n_stages;
+    int direct_in;    // stage 0 loads registers straight from HBM
+    int direct_out;   // last stage stores registers straight to HBM
+    int tiles_per_pe;
+    std::int8_t tile_pos[kTileBits];
+    std::int8_t outer_pos[64];
+    LightStage st[kLightMaxStages];
+    LightOp ops[kLightMaxOps];
+    double2 mats[kLightMaxMats];
+};
+
+void launch_light_pass(const LightParams& P, int total_tiles, cudaStream_t stream, int device);
+
+}  // namespace qrt

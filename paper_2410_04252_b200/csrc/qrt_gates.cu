@@ -457,6 +457,74 @@ bool env_on(const char* name, bool dflt) {
     return e ? std::atoi(e) != 0 : dflt;
 }
 
+// Merge the +-1 diagonal ops of one light stage (ops[begin, end)): every
+// thread-uniform sign op (kLSignU) commutes with all register work of the
+// stage, so they are pooled into as few ops as their fixed sources allow
+// (<= 6 W bits each) and placed first; consecutive slot-mask ops (kLSignS)
+// with <= 2 fixed sources together are combined.  Returns the new end.
+int merge_sign_ops(LightOp* ops, int begin, int end) {
+    auto bit_of = [](const LightOp& op, const std::vector<int>& F, int f) {
+        int fo = 0;  // the op's own fixed value from the merged value f
+        for (int i = 0; i < op.nsrc; ++i) {
+            const int at = static_cast<int>(std::find(F.begin(), F.end(), op.src[i]) - F.begin());
+            fo |= ((f >> at) & 1) << i;
+        }
+        return fo;
+    };
+    auto union_src = [](const std::vector<int>& F, const LightOp& op) {
+        std::vector<int> u = F;
+        for (int i = 0; i < op.nsrc; ++i)
+            if (std::find(u.begin(), u.end(), op.src[i]) == u.end()) u.push_back(op.src[i]);
+        return u;
+    };
+    auto finish = [](LightOp& m, const std::vector<int>& F) {
+        m.nsrc = static_cast<std::int8_t>(F.size());
+        for (std::size_t i = 0; i < F.size(); ++i) m.src[i] = static_cast<std::int8_t>(F[i]);
+    };
+    std::vector<LightOp> uni, rest;
+    for (int o = begin; o < end; ++o) (ops[o].kind == kLSignU ? uni : rest).push_back(ops[o]);
+    std::vector<LightOp> out;
+    // pooled uniform signs
+    for (std::size_t i = 0; i < uni.size();) {
+        std::vector<int> F;
+        std::size_t j = i;
+        while (j < uni.size() && union_src(F, uni[j]).size() <= 6) F = union_src(F, uni[j++]);
+        LightOp m = uni[i];
+        m.tab = 0;
+        for (int f = 0; f < (1 << F.size()); ++f) {
+            std::uint64_t b = 0;
+            for (std::size_t q = i; q < j; ++q) b ^= (uni[q].tab >> bit_of(uni[q], F, f)) & 1ull;
+            m.tab |= b << f;
+        }
+        finish(m, F);
+        out.push_back(m);
+        i = j;
+    }
+    // consecutive slot-mask signs
+    for (std::size_t i = 0; i < rest.size();) {
+        if (rest[i].kind != kLSignS) {
+            out.push_back(rest[i++]);
+            continue;
+        }
+        std::vector<int> F;
+        std::size_t j = i;
+        while (j < rest.size() && rest[j].kind == kLSignS && union_src(F, rest[j]).size() <= 2)
+            F = union_src(F, rest[j++]);
+        LightOp m = rest[i];
+        m.tab = 0;
+        for (int f = 0; f < (1 << F.size()); ++f) {
+            std::uint64_t mask = 0;
+            for (std::size_t q = i; q < j; ++q) mask ^= (rest[q].tab >> (16 * bit_of(rest[q], F, f))) & 0xffffull;
+            m.tab |= mask << (16 * f);
+        }
+        finish(m, F);
+        out.push_back(m);
+        i = j;
+    }
+    for (std::size_t i = 0; i < out.size(); ++i) ops[begin + static_cast<int>(i)] = out[i];
+    return begin + static_cast<int>(out.size());
+}
+
 // Stage plan of one light pass (see qrt_light.h): runs of the pass's ops,
 // each with four register positions S; dense targets lie in S, diagonal
 // gates anywhere; an op never overtakes a deferred op on a shared position.
@@ -857,6 +925,14 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
             if (s == 0) L->direct_in = (sbits & lowmask) == 0;
             if (s + 1 == stages.size()) L->direct_out = (sbits & lowmask) == 0;
             S.op_begin = static_cast<std::int16_t>(n_ops);
+            // W bit of a position: tile bit, or 12 + index among the outer positions
+            auto wbit = [&](int p) {
+                if (tb_of[p] >= 0) return tb_of[p];
+                for (int i = 0; i < no; ++i)
+                    if (L->outer_pos[i] == p) return kTileBits + i;
+                fail(QRT_ERR_INVALID, "light pass: diagonal target not in the local region");
+            };
+            int pend_bits = 0;  // register bits the pending slot signs depend on
             for (int id : stages[s].ops) {
                 const HostOp& o = opsv[static_cast<std::size_t>(id)];
                 LightOp& lo = L->ops[n_ops++];
@@ -867,12 +943,14 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
                 };
                 if (o.kind == kDense) {
                     const int qa = reg_of[tb_of[o.pos[0]]];
+                    int touched = 1 << qa;
                     if (o.k == 1) {
                         lo.kind = kL1;
                         lo.q0 = static_cast<std::int8_t>(qa);
                         put_mat(4, [&](int e) { return make_double2(o.m[2 * e], o.m[2 * e + 1]); });
                     } else {
                         const int qb = reg_of[tb_of[o.pos[1]]];
+                        touched |= 1 << qb;
                         lo.kind = kL2;
                         const bool swap = qa > qb;
                         lo.q0 = static_cast<std::int8_t>(swap ? qb : qa);
@@ -884,40 +962,62 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
                             return make_double2(o.m[2 * at], o.m[2 * at + 1]);
                         });
                     }
-                } else {
-                    lo.kind = o.sign ? kLSign : kLDiag;
-                    lo.neg = o.neg;
-                    for (int j = 0; j < kLightMaxDiagK; ++j) {
-                        lo.rq[j] = 4;
-                        lo.tb[j] = -1;
-                        lo.pos[j] = 0;
+                    // pending slot signs commute with this gate unless they
+                    // depend on one of its register bits
+                    if (pend_bits & touched) {
+                        lo.flush = 1;
+                        pend_bits = 0;
                     }
-                    for (int j = 0; j < o.k; ++j) {
-                        const int tb = tb_of[o.pos[j]];
-                        lo.tb[j] = static_cast<std::int8_t>(tb);
-                        lo.pos[j] = static_cast<std::int8_t>(o.pos[j]);
-                        lo.rq[j] = static_cast<std::int8_t>(tb >= 0 ? reg_of[tb] : 4);
-                    }
-                    if (!o.sign) put_mat(o.mat_len, [&](int e) { return make_double2(o.m[2 * e], o.m[2 * e + 1]); });
-                    if (o.sign) {  // tabulate negated register slots per value of the fixed bits
-                        int fixed_j[kLightMaxDiagK], nfix = 0;
-                        for (int j = 0; j < o.k; ++j)
-                            if (lo.rq[j] >= 4) fixed_j[nfix++] = j;
-                        if (nfix <= 2) {
-                            lo.q0 = 1;
-                            lo.negr = 0;
-                            for (int f = 0; f < (1 << nfix); ++f)
-                                for (int r = 0; r < 16; ++r) {
-                                    int m = 0;
-                                    for (int j = 0; j < o.k; ++j)
-                                        if (lo.rq[j] < 4) m |= ((r >> lo.rq[j]) & 1) << j;
-                                    for (int i = 0; i < nfix; ++i) m |= ((f >> i) & 1) << fixed_j[i];
-                                    if ((o.neg >> m) & 1ull) lo.negr |= 1ull << (16 * f + r);
-                                }
-                        }
+                    continue;
+                }
+                // diagonal: register targets and fixed (W-bit) sources
+                int nsrc = 0, regmask = 0;
+                for (int j = 0; j < kLightMaxDiagK; ++j) {
+                    lo.rq[j] = 4;
+                    lo.src[j] = 0;
+                    lo.fj[j] = 0;
+                }
+                for (int j = 0; j < o.k; ++j) {
+                    const int tb = tb_of[o.pos[j]];
+                    if (tb >= 0 && reg_of[tb] < 4) {
+                        lo.rq[j] = static_cast<std::int8_t>(reg_of[tb]);
+                        regmask |= 1 << reg_of[tb];
+                    } else {
+                        lo.src[nsrc] = static_cast<std::int8_t>(wbit(o.pos[j]));
+                        lo.fj[nsrc] = static_cast<std::int8_t>(j);
+                        ++nsrc;
                     }
                 }
+                lo.nsrc = static_cast<std::int8_t>(nsrc);
+                auto entry_index = [&](int f, int r) {
+                    int m = 0;
+                    for (int i = 0; i < nsrc; ++i) m |= ((f >> i) & 1) << lo.fj[i];
+                    for (int j = 0; j < o.k; ++j)
+                        if (lo.rq[j] < 4) m |= ((r >> lo.rq[j]) & 1) << j;
+                    return m;
+                };
+                if (!o.sign) {  // phase diagonal (k <= 2): commutes with pending signs
+                    lo.kind = kLDiag;
+                    put_mat(o.mat_len, [&](int e) { return make_double2(o.m[2 * e], o.m[2 * e + 1]); });
+                } else if (regmask == 0) {
+                    lo.kind = kLSignU;
+                    lo.tab = 0;
+                    for (int f = 0; f < (1 << nsrc); ++f)
+                        if ((o.neg >> entry_index(f, 0)) & 1ull) lo.tab |= 1ull << f;
+                } else if (nsrc <= 2) {
+                    lo.kind = kLSignS;
+                    lo.tab = 0;
+                    for (int f = 0; f < (1 << nsrc); ++f)
+                        for (int r = 0; r < 16; ++r)
+                            if ((o.neg >> entry_index(f, r)) & 1ull) lo.tab |= 1ull << (16 * f + r);
+                    pend_bits |= regmask;
+                } else {
+                    lo.kind = kLSignG;
+                    lo.tab = o.neg;
+                    pend_bits |= regmask;
+                }
             }
+            if (env_on("QRT_MERGE_SIGNS", true)) n_ops = merge_sign_ops(L->ops, S.op_begin, n_ops);
             S.op_count = static_cast<std::int16_t>(n_ops - S.op_begin);
         }
         if (n_ops > kLightMaxOps || n_mats > kLightMaxMats) fail(QRT_ERR_INVALID, "light pass over budget");

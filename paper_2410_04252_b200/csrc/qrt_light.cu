@@ -88,12 +88,32 @@ __device__ __forceinline__ void apply_signs(double2 (&a)[16], unsigned& pend) {
     pend = 0;
 }
 
-// Diagonal-entry index of register slot r: fixed bits | register bits.
-__device__ __forceinline__ int diag_index(int fixed, int r, const int (&rq)[kLightMaxDiagK], int k) {
-    int m = fixed;
-#pragma unroll
-    for (int j = 0; j < kLightMaxDiagK; ++j)
-        if (j < k) m |= ((r >> rq[j]) & 1) << j;
+// Pending +-1 signs folded into the slot mask: the thread-uniform bit g
+// flips every slot.
+__device__ __forceinline__ void flush_all(double2 (&a)[16], unsigned& pend, unsigned& g) {
+    pend ^= 0u - g;
+    g = 0;
+    apply_signs(a, pend);
+}
+
+// Value of the fixed (non-register) targets of a diagonal op: bit i = bit
+// src[i] of the thread word W.
+__device__ __forceinline__ int fixed_value(const LightOp& op, std::uint64_t W) {
+    const int ns = op.nsrc;
+    int f = 0;
+    if (ns > 0) f |= static_cast<int>((W >> op.src[0]) & 1ull);
+    if (ns > 1) f |= static_cast<int>((W >> op.src[1]) & 1ull) << 1;
+    for (int i = 2; i < ns; ++i) f |= static_cast<int>((W >> op.src[i]) & 1ull) << i;
+    return f;
+}
+
+// Diagonal index of slot r: fixed targets from f, register targets from r.
+__device__ __forceinline__ int diag_index(const LightOp& op, int f, int r) {
+    int m = 0;
+    const int k = op.k, ns = op.nsrc;
+    for (int i = 0; i < ns; ++i) m |= ((f >> i) & 1) << op.fj[i];
+    for (int j = 0; j < k; ++j)
+        if (op.rq[j] < 4) m |= ((r >> op.rq[j]) & 1) << j;
     return m;
 }
 
@@ -105,15 +125,13 @@ __global__ void __launch_bounds__(kLightThreads, 2) light_pass_kernel(const __gr
     const int c = P.c;
     const int t = threadIdx.x;
     u64 cta = 0;
-    {
-        const u64 b = static_cast<u64>(blockIdx.x % P.tiles_per_pe);
-        for (int i = 0; i < P.n_outer; ++i) cta |= ((b >> i) & 1ull) << P.outer_pos[i];
-    }
+    const u64 b = static_cast<u64>(blockIdx.x % P.tiles_per_pe);  // bit i <-> outer_pos[i]
+    for (int i = 0; i < P.n_outer; ++i) cta |= ((b >> i) & 1ull) << P.outer_pos[i];
+    const u64 wout = b << kTileBits;  // outer bits of the thread word W
     amp_t* __restrict__ v = P.ptrs[blockIdx.x / P.tiles_per_pe];
     const int nt = 1 << (kTileBits - c);
     const int cmask = (1 << c) - 1;
-    const bool staged_io = !P.direct_in || !P.direct_out;
-    if (staged_io) {
+    if (!P.direct_in || !P.direct_out) {
         for (int h = t; h < nt; h += kLightThreads) {
             u64 o = 0;
             for (int i = c; i < kTileBits; ++i) o |= static_cast<u64>((h >> (i - c)) & 1) << P.tile_pos[i];
@@ -123,22 +141,22 @@ __global__ void __launch_bounds__(kLightThreads, 2) light_pass_kernel(const __gr
     }
 
     double2 a[16];
-    unsigned pend = 0;   // pending sign flips (fast sign path)
-    // per-stage thread mapping
-    int ebase = 0;       // tile index of register slot 0
-    int sq[4];           // tile index of register bit q
+    unsigned pend = 0;  // pending slot signs
+    unsigned g = 0;     // pending thread-uniform sign
+    int ebase = 0;      // tile index of register slot 0
+    int swq[4];         // swizzled tile offset of register bit q (swz is linear over GF(2))
     auto map_stage = [&](const LightStage& S) {
         ebase = 0;
 #pragma unroll
         for (int i = 0; i < kTileBits - kLightRegBits; ++i) ebase |= ((t >> i) & 1) << S.tb[i];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) sq[q] = 1 << S.S[q];
+        for (int q = 0; q < 4; ++q) swq[q] = swz(1 << S.S[q]);
     };
-    auto slot_off = [&](int r) {  // tile-index offset of register slot r
-        int o = 0;
+    auto sslot = [&](int sb, int r) {
+        int o = sb;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            if ((r >> q) & 1) o |= sq[q];
+            if ((r >> q) & 1) o ^= swq[q];
         return o;
     };
     auto gofs = [&](int e) {  // tile index -> offset inside the PE
@@ -166,38 +184,48 @@ __global__ void __launch_bounds__(kLightThreads, 2) light_pass_kernel(const __gr
         }
     } else {
         for (int e = t; e < E; e += kLightThreads) {
-            const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(&tile[swz(e)]));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s),
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&tile[swz(e)]));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
                          "l"(&v[cta | tab[e >> c] | (e & cmask)]));
         }
         asm volatile("cp.async.wait_all;\n" ::);
         __syncthreads();
         const int sb = swz(ebase);
 #pragma unroll
-        for (int r = 0; r < 16; ++r) a[r] = tile[sb ^ swz(slot_off(r))];
+        for (int r = 0; r < 16; ++r) a[r] = tile[sslot(sb, r)];
     }
 
     for (int s = 0; s < P.n_stages; ++s) {
         const LightStage& S = P.st[s];
         if (s > 0) {
             // transpose through shared memory: previous mapping out, this one in
+            flush_all(a, pend, g);
             {
-                apply_signs(a, pend);
                 const int sb = swz(ebase);
                 __syncthreads();  // readers of the previous transpose are done
 #pragma unroll
-                for (int r = 0; r < 16; ++r) tile[sb ^ swz(slot_off(r))] = a[r];
+                for (int r = 0; r < 16; ++r) tile[sslot(sb, r)] = a[r];
             }
             __syncthreads();
             map_stage(S);
             const int sb = swz(ebase);
 #pragma unroll
-            for (int r = 0; r < 16; ++r) a[r] = tile[sb ^ swz(slot_off(r))];
+            for (int r = 0; r < 16; ++r) a[r] = tile[sslot(sb, r)];
         }
-        for (int o = S.op_begin; o < S.op_begin + S.op_count; ++o) {
+        const u64 W = static_cast<u64>(ebase) | wout;
+        const int o_end = S.op_begin + S.op_count;
+        for (int o = S.op_begin; o < o_end; ++o) {
             const LightOp& op = P.ops[o];
             const int kind = op.kind;
-            if (kind != kLSign && pend) apply_signs(a, pend);
+            if (kind == kLSignU) {
+                g ^= static_cast<unsigned>(op.tab >> fixed_value(op, W)) & 1u;
+                continue;
+            }
+            if (kind == kLSignS) {
+                pend ^= static_cast<unsigned>(op.tab >> (16 * fixed_value(op, W))) & 0xffffu;
+                continue;
+            }
+            if (op.flush) apply_signs(a, pend);
             if (kind == kL1) {
                 const double2* m = P.mats + op.mat;
                 switch (op.q0) {
@@ -208,57 +236,24 @@ __global__ void __launch_bounds__(kLightThreads, 2) light_pass_kernel(const __gr
                 }
             } else if (kind == kL2) {
                 apply_dense2(a, P.mats + op.mat, op.q0, op.q1);
+            } else if (kind == kLSignG) {
+                const int f = fixed_value(op, W);
+                unsigned mask = 0;
+#pragma unroll
+                for (int r = 0; r < 16; ++r) mask |= static_cast<unsigned>((op.tab >> diag_index(op, f, r)) & 1ull) << r;
+                pend ^= mask;
             } else {
-                const int k = op.k;
-                if (kind == kLSign && op.q0) {
-                    // fast path: the host tabulated the negated slots per value
-                    // of the (<= 2) non-register target bits
-                    int f = 0, i = 0;
-                    for (int j = 0; j < k; ++j) {
-                        if (op.rq[j] < 4) continue;
-                        const int tb = op.tb[j];
-                        const int bit = tb >= 0 ? (ebase >> tb) & 1 : static_cast<int>((cta >> op.pos[j]) & 1ull);
-                        f |= bit << i++;
-                    }
-                    pend ^= static_cast<unsigned>(op.negr >> (16 * f)) & 0xffffu;
-                } else if (kind == kLSign) {
-                    int fixed = 0, rq[kLightMaxDiagK];
-#pragma unroll
-                    for (int j = 0; j < kLightMaxDiagK; ++j) {
-                        rq[j] = op.rq[j];
-                        if (j < k && rq[j] >= 4) {
-                            const int tb = op.tb[j];
-                            const int bit = tb >= 0 ? (ebase >> tb) & 1 : static_cast<int>((cta >> op.pos[j]) & 1ull);
-                            fixed |= bit << j;
-                        }
-                    }
-                    const u64 neg = op.neg;
-                    unsigned mask = 0;
-#pragma unroll
-                    for (int r = 0; r < 16; ++r) mask |= static_cast<unsigned>((neg >> diag_index(fixed, r, rq, k)) & 1ull) << r;
-                    pend ^= mask;
-                } else {
-                    int fixed = 0, rq[kLightMaxDiagK];
-#pragma unroll
-                    for (int j = 0; j < kLightMaxDiagK; ++j) {
-                        rq[j] = op.rq[j];
-                        if (j < k && rq[j] >= 4) {
-                            const int tb = op.tb[j];
-                            const int bit = tb >= 0 ? (ebase >> tb) & 1 : static_cast<int>((cta >> op.pos[j]) & 1ull);
-                            fixed |= bit << j;
-                        }
-                    }
-                    // phase diagonal (k <= 2): two entries live at a time
-                    const double2* d = P.mats + op.mat;
-                    const int halves = k > 1 ? 2 : 1;
+                // phase diagonal (k <= 2): two entries live at a time
+                const int f = fixed_value(op, W);
+                const double2* d = P.mats + op.mat;
+                const int halves = op.k > 1 ? 2 : 1;
 #pragma unroll 1
-                    for (int hb = 0; hb < halves; ++hb) {
-                        const double2 d0 = d[2 * hb], d1 = d[2 * hb + 1];
+                for (int hb = 0; hb < halves; ++hb) {
+                    const double2 d0 = d[2 * hb], d1 = d[2 * hb + 1];
 #pragma unroll
-                        for (int r = 0; r < 16; ++r) {
-                            const int m = diag_index(fixed, r, rq, k);
-                            if ((m >> 1) == hb) a[r] = cmul((m & 1) ? d1 : d0, a[r]);
-                        }
+                    for (int r = 0; r < 16; ++r) {
+                        const int m = diag_index(op, f, r);
+                        if ((m >> 1) == hb) a[r] = cmul((m & 1) ? d1 : d0, a[r]);
                     }
                 }
             }
@@ -266,7 +261,7 @@ __global__ void __launch_bounds__(kLightThreads, 2) light_pass_kernel(const __gr
     }
 
     // ---- last stage output
-    apply_signs(a, pend);
+    flush_all(a, pend, g);
     if (P.direct_out) {
         const u64 g0 = gofs(ebase);
         u64 gq[4];
@@ -284,7 +279,7 @@ __global__ void __launch_bounds__(kLightThreads, 2) light_pass_kernel(const __gr
         const int sb = swz(ebase);
         __syncthreads();
 #pragma unroll
-        for (int r = 0; r < 16; ++r) tile[sb ^ swz(slot_off(r))] = a[r];
+        for (int r = 0; r < 16; ++r) tile[sslot(sb, r)] = a[r];
         __syncthreads();
         for (int e = t; e < E; e += kLightThreads) __stcs(&v[cta | tab[e >> c] | (e & cmask)], tile[swz(e)]);
     }

@@ -155,3 +155,30 @@ def test_light_pass_count_and_launches(qb, device):
     qb.apply_gates_narrow(st, c, list(range(c.size())))
     g = st.stats()["gates"]
     assert 0 < g["launches"] <= c.size() // 8, g
+
+
+@pytest.mark.parametrize("merge", ["0", "1"])
+def test_light_sign_merging(qb, device, merge, monkeypatch):
+    """CZ/CCZ-heavy runs with sign-op pooling on and off (QRT_MERGE_SIGNS)."""
+    monkeypatch.setenv("QRT_MERGE_SIGNS", merge)
+    rng = np.random.default_rng(404)
+    n, p = 17, 2
+    nl = n - 1
+    ops = []
+    for i in range(500):
+        if rng.random() < 0.25:
+            ops.append(qb.make_gate(i, [int(rng.integers(nl))], qb.random_unitary(1, int(rng.integers(1 << 62)))))
+        else:
+            k = int(rng.integers(1, 4))
+            targets = [int(x) for x in rng.choice(nl, size=k, replace=False)]
+            d = np.ones(1 << k, dtype=complex)
+            d[-1] = -1  # CZ / CCZ / Z
+            ops.append(qb.make_gate(i, targets, np.diag(d)))
+    circ = qb.Circuit(n, ops)
+    psi = qb.random_state(n, 404)
+    st = qb.init_state_from(psi, qb.ClusterShape.flat(p))
+    qb.apply_gates_narrow(st, circ, list(range(len(ops))))
+    sub = psi.reshape(p, -1).copy()
+    for op in ops:
+        cpu.apply_gate(sub, list(op.targets), op.payload)
+    assert float(np.max(np.abs(_sub(st) - sub))) <= AMP_TOL

@@ -26,7 +26,7 @@ CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = str(CUDA_HOME / "bin" / "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SRCS = ["qrt_abi.cu", "qrt_gates.cu", "qrt_light.cu", "qrt_reorder.cu", "qrt_pauli.cu"]
+CU_SRCS = ["qrt_abi.cu", "qrt_gates.cu", "qrt_light.cu", "qrt_reorder.cu", "qrt_pauli.cu", "qrt_coset.cu"]
 HOST_SRCS = ["qubit_core.cpp", "relayout.cpp", "tiling_qsu.cpp", "tiling_evc.cpp", "generators.cpp",
              "device_state.cpp"]
 

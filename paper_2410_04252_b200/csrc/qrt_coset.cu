@@ -1,0 +1,231 @@
+// libqrt — register-coset EVC pass kernel (see qrt_coset.h).
+//
+// Reference semantics: per PE, partial[pe] += sum_t coeff_t * pe_sign_t *
+// local_pauli_expectation(sub[pe], mask_t)  (dist_sim.cpp:84-97, 289-295),
+// evaluated pair-wise over the canonical half of each flip-mask group.
+// One CTA = one 2^12-amplitude tile = 128 threads x 32-amplitude cosets.
+
+#include "qrt_coset.h"
+
+namespace qrt {
+
+namespace {
+
+using u64 = std::uint64_t;
+
+__device__ __forceinline__ int swz(int e) {
+    const int x = e >> 3;
+    return e ^ ((x ^ (x >> 3) ^ (x >> 6) ^ (x >> 9)) & 7);
+}
+
+__device__ __forceinline__ int insert_zero(int v, int bit) {
+    return ((v >> bit) << (bit + 1)) | (v & ((1 << bit) - 1));
+}
+
+__host__ __device__ constexpr int top_bit(int v) { return v >= 16 ? 4 : v >= 8 ? 3 : v >= 4 ? 2 : v >= 2 ? 1 : 0; }
+__host__ __device__ constexpr int ins0(int v, int bit) { return ((v >> bit) << (bit + 1)) | (v & ((1 << bit) - 1)); }
+
+// sum_rho T[rho] * Re(conj(a[r^XQ]) a[r]) over the 16 canonical pairs
+// (r, r^XQ) of the coset, r without the top bit of XQ (register indices are
+// compile-time: one code body per mask).
+template <int XQ>
+__device__ __forceinline__ double coset_group(const double2 (&a)[32], const double* __restrict__ T) {
+    constexpr int H = top_bit(XQ);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int rho = 0; rho < 16; ++rho) {
+        const int r = ins0(rho, H);
+        const int s = r ^ XQ;
+        const double2 A = a[s], B = a[r];
+        acc[rho & 3] = fma(T[rho], fma(A.x, B.x, A.y * B.y), acc[rho & 3]);
+    }
+    return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
+// Any flip mask / table mode, pairs read from the shared-memory tile
+// (groups outside the Jordan-Wigner fast set: odd weights, Im(w) terms,
+// complex coefficients).
+__device__ __noinline__ double2 coset_generic(const double2* __restrict__ tile, int sb, const int* swq, int xq,
+                                              int mode, const double* __restrict__ T) {
+    const int H = 31 - __clz(xq);
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 1
+    for (int rho = 0; rho < 16; ++rho) {
+        const int r = insert_zero(rho, H), s = r ^ xq;
+        int orr = sb, os = sb;
+        for (int q = 0; q < kCosetBits; ++q) {
+            if ((r >> q) & 1) orr ^= swq[q];
+            if ((s >> q) & 1) os ^= swq[q];
+        }
+        const double2 A = tile[os], B = tile[orr];
+        const double re = fma(A.x, B.x, A.y * B.y);
+        if (mode == 0) {
+            acc.x = fma(T[rho], re, acc.x);
+        } else {
+            const double im = fma(A.x, B.y, -A.y * B.x);
+            acc.x = fma(T[rho], re, fma(T[32 + rho], im, acc.x));
+            acc.y = fma(T[16 + rho], re, fma(T[48 + rho], im, acc.y));
+        }
+    }
+    return acc;
+}
+
+// The fast groups of a coset set (Re(w) only, real coefficients, flip
+// masks of weight 2 or 4) are sorted by mask: [xbeg[x-1], xbeg[x]) have mask
+// x.  The 15 masks are walked in a fixed unrolled order (one code body per
+// mask, no switch), so the coset stays in registers.
+template <int XQ>
+__device__ __forceinline__ void coset_fast(const double2 (&a)[32], const CosetParams& P, const CosetSet& S,
+                                           std::uint64_t W, std::uint64_t pe, double2& acc) {
+    const int g0 = S.g_begin + S.xbeg[XQ - 1], g1 = S.g_begin + S.xbeg[XQ];
+    for (int g = g0; g < g1; ++g) {
+        const CosetGroup& G = P.groups[g];
+        const double r = coset_group<XQ>(a, P.tabs + G.tab);
+        const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
+        acc.x += odd ? -r : r;
+    }
+}
+
+__device__ __forceinline__ double2 block_sum(double2 v, double2* scratch) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v.x += __shfl_down_sync(0xffffffffu, v.x, o);
+        v.y += __shfl_down_sync(0xffffffffu, v.y, o);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    double2 r = make_double2(0.0, 0.0);
+    if (threadIdx.x == 0)
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            r.x += scratch[w].x;
+            r.y += scratch[w].y;
+        }
+    return r;
+}
+
+__global__ void __launch_bounds__(kCosetThreads, 2)
+    coset_pass_kernel(const __grid_constant__ CosetParams P, const CosetDiagTerm* __restrict__ dterms,
+                      double* __restrict__ red) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double2 scratch[kCosetThreads / 32];
+    constexpr int E = 1 << kTileBits;
+    const int c = P.c, t = threadIdx.x;
+    double2* tile = reinterpret_cast<double2*>(smem_raw);
+    u64* tabo = reinterpret_cast<u64*>(tile + E);
+    double* Wsh = reinterpret_cast<double*>(tabo + (1 << (kTileBits - c)));
+
+    const u64 b = static_cast<u64>(blockIdx.x);  // bit i <-> outer_pos[i]
+    u64 base = 0;
+    for (int i = 0; i < P.n_outer; ++i) base |= ((b >> i) & 1ull) << P.outer_pos[i];
+    for (int h = t; h < (1 << (kTileBits - c)); h += kCosetThreads) {
+        u64 o = 0;
+        for (int i = c; i < kTileBits; ++i) o |= static_cast<u64>((h >> (i - c)) & 1) << P.tile_pos[i];
+        tabo[h] = o;
+    }
+    __syncthreads();
+    const amp_t* __restrict__ v = P.ptrs[blockIdx.y];
+    const u64 pe = static_cast<u64>(P.pe_begin) + blockIdx.y;
+    const int cmask = (1 << c) - 1;
+    for (int e = t; e < E; e += kCosetThreads) {
+        const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&tile[swz(e)]));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(&v[base | tabo[e >> c] | (e & cmask)]));
+    }
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
+
+    double2 acc = make_double2(0.0, 0.0);
+    if (P.d_count > 0) {  // I/Z words: Walsh-Hadamard transform of |v|^2 over the tile
+        for (int e = t; e < E; e += kCosetThreads) {
+            const double2 a = tile[swz(e)];
+            Wsh[e] = fma(a.x, a.x, a.y * a.y);
+        }
+        __syncthreads();
+        for (int s = 0; s < kTileBits; ++s) {
+            for (int i = t; i < (E >> 1); i += kCosetThreads) {
+                const int i0 = insert_zero(i, s), i1 = i0 | (1 << s);
+                const double x = Wsh[i0], y = Wsh[i1];
+                Wsh[i0] = x + y;
+                Wsh[i1] = x - y;
+            }
+            __syncthreads();
+        }
+        for (int k = t; k < P.d_count; k += kCosetThreads) {
+            const CosetDiagTerm tm = dterms[P.d_begin + k];
+            const int odd = (__popcll(base & tm.m) + __popcll(pe & tm.gz)) & 1;
+            const double val = odd ? -Wsh[tm.m_tile] : Wsh[tm.m_tile];
+            acc.x = fma(tm.f.x, val, acc.x);
+            acc.y = fma(tm.f.y, val, acc.y);
+        }
+    }
+
+    const u64 wout = b << kTileBits;
+    for (int s = 0; s < P.n_sets; ++s) {
+        const CosetSet& S = P.sets[s];
+        int ebase = 0;
+#pragma unroll
+        for (int i = 0; i < kTileBits - kCosetBits; ++i) ebase |= ((t >> i) & 1) << S.tb[i];
+        int swq[kCosetBits];
+#pragma unroll
+        for (int q = 0; q < kCosetBits; ++q) swq[q] = swz(1 << S.S[q]);
+        const int sb = swz(ebase);
+        double2 a[32];
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+            int o = sb;
+#pragma unroll
+            for (int q = 0; q < kCosetBits; ++q)
+                if ((r >> q) & 1) o ^= swq[q];
+            a[r] = tile[o];
+        }
+        const u64 W = static_cast<u64>(ebase) | wout;
+        coset_fast<3>(a, P, S, W, pe, acc);
+        coset_fast<5>(a, P, S, W, pe, acc);
+        coset_fast<6>(a, P, S, W, pe, acc);
+        coset_fast<9>(a, P, S, W, pe, acc);
+        coset_fast<10>(a, P, S, W, pe, acc);
+        coset_fast<12>(a, P, S, W, pe, acc);
+        coset_fast<15>(a, P, S, W, pe, acc);
+        coset_fast<17>(a, P, S, W, pe, acc);
+        coset_fast<18>(a, P, S, W, pe, acc);
+        coset_fast<20>(a, P, S, W, pe, acc);
+        coset_fast<23>(a, P, S, W, pe, acc);
+        coset_fast<24>(a, P, S, W, pe, acc);
+        coset_fast<27>(a, P, S, W, pe, acc);
+        coset_fast<29>(a, P, S, W, pe, acc);
+        coset_fast<30>(a, P, S, W, pe, acc);
+        for (int g = S.g_begin + S.xbeg[31]; g < S.g_begin + S.g_count; ++g) {
+            const CosetGroup& G = P.groups[g];
+            const double2 r = coset_generic(tile, sb, swq, G.xq, G.mode, P.tabs + G.tab);
+            const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
+            acc.x += odd ? -r.x : r.x;
+            acc.y += odd ? -r.y : r.y;
+        }
+    }
+    const double2 tot = block_sum(acc, scratch);
+    if (t == 0) {
+        double* slot = red + 2 * (static_cast<std::size_t>(blockIdx.y) * gridDim.x + blockIdx.x);
+        slot[0] += tot.x;
+        slot[1] += tot.y;
+    }
+}
+
+}  // namespace
+
+void launch_coset_pass(const CosetParams& P, const CosetDiagTerm* dterms, int pe_count, double* red,
+                       cudaStream_t stream, int device) {
+    static bool attr_done[64] = {};
+    if (!attr_done[device]) {
+        QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
+        attr_done[device] = true;
+    }
+    const std::size_t smem = (std::size_t{1} << kTileBits) * sizeof(double2) +
+                             (std::size_t{1} << (kTileBits - P.c)) * sizeof(std::uint64_t) +
+                             (P.d_count > 0 ? (std::size_t{1} << kTileBits) * sizeof(double) : 0);
+    dim3 grid(static_cast<unsigned>(P.tiles_per_pe), static_cast<unsigned>(pe_count));
+    coset_pass_kernel<<<grid, kCosetThreads, smem, stream>>>(P, dterms, red);
+    QRT_CUDA(cudaGetLastError());
+}
+
+}  // namespace qrt

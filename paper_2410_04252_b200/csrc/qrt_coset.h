@@ -1,0 +1,75 @@
+// libqrt — register-coset EVC passes (reference local_pauli_expectation +
+// expectation, dist_sim.cpp:84-97 and :289-298).  Shared by the host planner
+// (qrt_pauli.cu) and the kernel (qrt_coset.cu).
+//
+// A pass loads a 2^12-amplitude tile (positions B) into shared memory once.
+// Its flip-mask groups are covered by *cosets*: five tile bits Q; every
+// thread of the 128-thread CTA then holds the 32 amplitudes of one coset of
+// Q in registers and evaluates every group whose flip mask x lies in Q from
+// registers alone: for the 16 canonical pairs (r, r^x) of the coset
+//   sum_t F_t s_t(i) comp_t(conj(v[i^x]) v[i])
+//     = sigma(thread) * sum_rho C[rho] * comp(conj(a[r^x]) a[r]),
+// where the 16-entry table C folds every term's sign over the register bits
+// and sigma = (-1)^{popc(W & mf) + popc(pe & gz)} is the sign over the bits
+// outside Q, common to the group's terms (the host splits a group when it is
+// not).  For Jordan-Wigner words (Re(w) only, real coefficients) a pair costs
+// three fp64 instructions, and one shared-memory read of a coset (16 B per
+// amplitude) serves up to C(5,4)+C(5,2) = 15 groups.
+#pragma once
+
+#include <cstdint>
+
+#include "qrt_internal.h"
+
+namespace qrt {
+
+inline constexpr int kCosetBits = 5;                                  // 32 amplitudes per thread
+inline constexpr int kCosetThreads = 1 << (kTileBits - kCosetBits);   // 128
+inline constexpr int kCosetMaxSets = 40;
+inline constexpr int kCosetMaxGroups = 320;
+inline constexpr int kCosetMaxTab = 2048;  // doubles in the launch parameters
+
+struct CosetGroup {
+    std::uint64_t mf;  // sign bits outside Q, as bits of the thread word W
+    std::uint64_t gz;  // sign bits over the PE index
+    std::int16_t tab;  // first double of the group's table(s) in CosetParams::tabs
+    std::int8_t xq;    // flip mask over the coset's register bits (nonzero)
+    std::int8_t mode;  // 0: Re(w) only with real coefficients (16 doubles), 1: general (64 doubles)
+};
+
+struct CosetSet {
+    std::int8_t S[kCosetBits];                // tile bit of register bit q
+    std::int8_t tb[kTileBits - kCosetBits];   // tile bit of thread-index bit i
+    std::int16_t g_begin, g_count;
+    std::uint8_t xbeg[32];  // fast groups sorted by mask: [xbeg[x-1], xbeg[x]) have mask x; generic from xbeg[31]
+};
+
+// W = tile index (bits 0..11) | outer index of the CTA (bit 12 + i <-> outer_pos[i]).
+struct CosetParams {
+    const amp_t* ptrs[kMaxLocalPEs];
+    int c;
+    int n_outer;
+    int n_sets;
+    int pe_begin;
+    int tiles_per_pe;
+    int d_begin, d_count;  // I/Z words of this pass (global term array), Walsh-Hadamard path
+    std::int8_t tile_pos[kTileBits];
+    std::int8_t outer_pos[64];
+    CosetSet sets[kCosetMaxSets];
+    CosetGroup groups[kCosetMaxGroups];
+    double tabs[kCosetMaxTab];
+};
+
+// I/Z word of the Walsh-Hadamard path (same layout as the tiled EVC kernel's).
+struct CosetDiagTerm {
+    std::uint64_t m;   // full sign mask (local positions)
+    std::uint64_t gz;  // PE-index sign mask
+    double2 f;         // coefficient
+    int m_tile;        // sign mask bits inside the tile, tile-bit indices
+    int pad;
+};
+
+void launch_coset_pass(const CosetParams& P, const CosetDiagTerm* dterms, int pe_count, double* red,
+                       cudaStream_t stream, int device);
+
+}  // namespace qrt

@@ -23,10 +23,13 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 
-#include "qrt_internal.h"
+#include "qrt_coset.h"
 
 namespace qrt {
 
@@ -442,9 +445,273 @@ struct PauliPlanHost {
     int T = 0;
     std::vector<PGroup> dgroups;
     std::vector<PTerm> dterms;
-    std::vector<PPass> hdrs;
+    std::vector<PPass> hdrs;  // tiled passes (shared-memory pair loop)
     std::vector<WGroup> wgroups;
+    std::vector<std::unique_ptr<CosetParams>> cosets;  // register-coset passes
+    std::vector<CosetDiagTerm> cdterms;
+    int coset_sets = 0;
 };
+
+namespace {
+
+bool coset_enabled() {
+    const char* e = std::getenv("QRT_EVC_COSET");
+    return e ? std::atoi(e) != 0 : true;
+}
+
+// Builds the register-coset launches of one tile pass (positions B; flip-mask
+// groups `gidx` into `flips`, each with its terms; `diag` I/Z terms if any).
+// Groups are covered greedily by 5-bit register sets Q; within a set each
+// group is split by the sign bits its terms have outside Q (so that one
+// thread sign serves all of them) and folded into a 16-entry table.
+void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B,
+                      const std::vector<std::pair<std::uint64_t, std::vector<int>>>& flips, const std::vector<int>& gidx,
+                      const std::vector<int>& diag, const std::uint64_t* y, const std::uint64_t* z,
+                      const std::uint64_t* gz, const double* coeffs) {
+    int tile_pos[kTileBits], outer_pos[64], tb_of[64], ob_of[64];
+    int ti = 0, no = 0;
+    for (int p = 0; p < 64; ++p) tb_of[p] = ob_of[p] = -1;
+    for (int p = 0; p < nl; ++p) {
+        if (B >> p & 1ull) {
+            tb_of[p] = ti;
+            tile_pos[ti++] = p;
+        } else {
+            ob_of[p] = no;
+            outer_pos[no++] = p;
+        }
+    }
+    int c = 0;
+    while (c < kTileBits && tile_pos[c] == c) ++c;
+    auto to_tile = [&](std::uint64_t m) {
+        int r = 0;
+        for (int i = 0; i < kTileBits; ++i) r |= static_cast<int>((m >> tile_pos[i]) & 1ull) << i;
+        return r;
+    };
+    auto fresh = [&]() {
+        auto P = std::make_unique<CosetParams>();
+        std::memset(P.get(), 0, sizeof(CosetParams));
+        P->c = c;
+        P->n_outer = no;
+        P->pe_begin = pe_begin;
+        P->tiles_per_pe = 1 << (nl - kTileBits);
+        for (int i = 0; i < kTileBits; ++i) P->tile_pos[i] = static_cast<std::int8_t>(tile_pos[i]);
+        for (int i = 0; i < no; ++i) P->outer_pos[i] = static_cast<std::int8_t>(outer_pos[i]);
+        return P;
+    };
+    auto P = fresh();
+    int n_groups = 0, n_tab = 0;
+    if (!diag.empty()) {
+        P->d_begin = static_cast<int>(plan.cdterms.size());
+        P->d_count = static_cast<int>(diag.size());
+        for (int t : diag) {
+            CosetDiagTerm tm{};
+            tm.m = z[t] | y[t];
+            tm.gz = gz[t];
+            tm.f = make_double2(coeffs[2 * t], coeffs[2 * t + 1]);
+            tm.m_tile = to_tile(tm.m & B);
+            plan.cdterms.push_back(tm);
+        }
+    }
+    // tile-bit flip masks of the groups
+    std::vector<int> left = gidx;
+    std::vector<int> xt(flips.size(), 0);
+    for (int g : gidx) xt[static_cast<std::size_t>(g)] = to_tile(flips[static_cast<std::size_t>(g)].first);
+    std::stable_sort(left.begin(), left.end(), [&](int a, int b) {
+        return __builtin_popcount(static_cast<unsigned>(xt[static_cast<std::size_t>(a)])) >
+               __builtin_popcount(static_cast<unsigned>(xt[static_cast<std::size_t>(b)]));
+    });
+    while (!left.empty()) {
+        // ---- choose Q: 5 tile bits covering most remaining groups
+        int bestQ = 0, best = -1;
+        const std::size_t seeds = std::min<std::size_t>(12, left.size());
+        for (std::size_t sd = 0; sd < seeds; ++sd) {
+            const int x = xt[static_cast<std::size_t>(left[sd])];
+            const int need = kCosetBits - __builtin_popcount(static_cast<unsigned>(x));
+            std::vector<int> free;
+            for (int b = 0; b < kTileBits; ++b)
+                if (!(x >> b & 1)) free.push_back(b);
+            // all ways to add `need` bits (<= C(11,4) = 330)
+            std::vector<int> pick(static_cast<std::size_t>(need));
+            for (int i = 0; i < need; ++i) pick[static_cast<std::size_t>(i)] = i;
+            const int F = static_cast<int>(free.size());
+            while (true) {
+                int Q = x;
+                for (int i = 0; i < need; ++i) Q |= 1 << free[static_cast<std::size_t>(pick[static_cast<std::size_t>(i)])];
+                int cnt = 0;
+                for (int g : left) cnt += (xt[static_cast<std::size_t>(g)] & ~Q) == 0;
+                if (cnt > best) {
+                    best = cnt;
+                    bestQ = Q;
+                }
+                int i = need - 1;
+                while (i >= 0 && pick[static_cast<std::size_t>(i)] == F - need + i) --i;
+                if (i < 0) break;
+                ++pick[static_cast<std::size_t>(i)];
+                for (int j = i + 1; j < need; ++j) pick[static_cast<std::size_t>(j)] = pick[static_cast<std::size_t>(j - 1)] + 1;
+            }
+        }
+        std::vector<int> in, keep;
+        for (int g : left) ((xt[static_cast<std::size_t>(g)] & ~bestQ) == 0 ? in : keep).push_back(g);
+        left.swap(keep);
+        // ---- the set: register bits, thread bits (conflict-free lanes)
+        CosetSet S{};
+        int reg_of[kTileBits];
+        {
+            int q = 0;
+            for (int i = 0; i < kTileBits; ++i) {
+                reg_of[i] = -1;
+                if (bestQ >> i & 1) {
+                    S.S[q] = static_cast<std::int8_t>(i);
+                    reg_of[i] = q++;
+                }
+            }
+            std::vector<int> rest, lead;
+            for (int i = 0; i < kTileBits; ++i)
+                if (!(bestQ >> i & 1)) rest.push_back(i);
+            for (int res = 0; res < 3; ++res)
+                for (std::size_t u = 0; u < rest.size(); ++u)
+                    if (rest[u] % 3 == res) {
+                        lead.push_back(rest[u]);
+                        rest.erase(rest.begin() + static_cast<std::ptrdiff_t>(u));
+                        break;
+                    }
+            rest.insert(rest.begin(), lead.begin(), lead.end());
+            for (int i = 0; i < kTileBits - kCosetBits; ++i) S.tb[i] = static_cast<std::int8_t>(rest[static_cast<std::size_t>(i)]);
+        }
+        auto to_reg = [&](int tilemask) {
+            int r = 0;
+            for (int i = 0; i < kTileBits; ++i)
+                if ((tilemask >> i & 1) && reg_of[i] >= 0) r |= 1 << reg_of[i];
+            return r;
+        };
+        // W-bit mask of sign bits outside Q
+        auto to_w = [&](std::uint64_t m) {
+            std::uint64_t w = 0;
+            for (int p = 0; p < nl; ++p) {
+                if (!(m >> p & 1ull)) continue;
+                if (tb_of[p] >= 0) {
+                    if (!(bestQ >> tb_of[p] & 1)) w |= 1ull << tb_of[p];
+                } else {
+                    w |= 1ull << (kTileBits + ob_of[p]);
+                }
+            }
+            return w;
+        };
+        // ---- groups of the set, sorted by register flip mask, split by outside signs
+        struct Sub {
+            int xq;
+            std::uint64_t mf, gz;
+            std::vector<int> terms;
+        };
+        std::vector<Sub> subs;
+        for (int g : in) {
+            const int xq = to_reg(xt[static_cast<std::size_t>(g)]);
+            for (int t : flips[static_cast<std::size_t>(g)].second) {
+                const std::uint64_t m = z[t] | y[t];
+                const std::uint64_t mf = to_w(m);
+                auto it = std::find_if(subs.begin(), subs.end(), [&](const Sub& u) {
+                    return u.xq == xq && u.mf == mf && u.gz == gz[t];
+                });
+                if (it == subs.end()) {
+                    subs.push_back(Sub{xq, mf, gz[t], {}});
+                    it = subs.end() - 1;
+                }
+                it->terms.push_back(t);
+            }
+        }
+        // fast subgroups (Re(w) only, real coefficients, weight-2/4 masks)
+        // first, sorted by mask; the generic ones after them
+        auto fast_of = [&](const Sub& u) {
+            const int w = __builtin_popcount(static_cast<unsigned>(u.xq));
+            if (w != 2 && w != 4) return false;
+            for (int t : u.terms)
+                if ((__builtin_popcountll(y[t]) & 1) || coeffs[2 * t + 1] != 0.0) return false;
+            return true;
+        };
+        std::stable_sort(subs.begin(), subs.end(), [&](const Sub& a, const Sub& b) {
+            const bool fa = fast_of(a), fb = fast_of(b);
+            if (fa != fb) return fa;
+            return fa && a.xq < b.xq;
+        });
+        // emit in chunks that fit the launch parameters (a set whose
+        // subgroups overflow one launch is repeated with the same Q)
+        auto re_real_of = [&](const Sub& u) {
+            for (int t : u.terms)
+                if ((__builtin_popcountll(y[t]) & 1) || coeffs[2 * t + 1] != 0.0) return false;
+            return true;
+        };
+        std::size_t at = 0;
+        while (at < subs.size()) {
+            auto room = [&](std::size_t from) {
+                std::size_t end = from;
+                int g = n_groups, tb = n_tab;
+                while (end < subs.size() && end - from < 255) {
+                    const int need = re_real_of(subs[end]) ? 16 : 64;
+                    if (g + 1 > kCosetMaxGroups || tb + need > kCosetMaxTab) break;
+                    ++g;
+                    tb += need;
+                    ++end;
+                }
+                return end;
+            };
+            std::size_t end = room(at);
+            if (end == at || P->n_sets >= kCosetMaxSets) {
+                plan.cosets.push_back(std::move(P));
+                P = fresh();
+                n_groups = n_tab = 0;
+                end = room(at);
+                if (end == at) fail(QRT_ERR_INVALID, "EVC coset group exceeds the launch budget");
+            }
+            CosetSet Sc = S;
+            Sc.g_begin = static_cast<std::int16_t>(n_groups);
+            Sc.g_count = static_cast<std::int16_t>(end - at);
+            for (int xq = 0; xq < 32; ++xq) {
+                int cnt = 0;
+                for (std::size_t q = at; q < end; ++q) cnt += fast_of(subs[q]) && subs[q].xq <= xq;
+                Sc.xbeg[xq] = static_cast<std::uint8_t>(cnt);  // fast subgroups with mask <= xq
+            }
+            for (std::size_t q = at; q < end; ++q) {
+                const Sub& u = subs[q];
+                CosetGroup& G = P->groups[n_groups++];
+                G.xq = static_cast<std::int8_t>(u.xq);
+                G.mf = u.mf;
+                G.gz = u.gz;
+                G.tab = static_cast<std::int16_t>(n_tab);
+                const bool re_real = re_real_of(u);
+                G.mode = re_real ? 0 : 1;
+                const int H = 31 - __builtin_clz(static_cast<unsigned>(u.xq));
+                double* T = P->tabs + n_tab;
+                n_tab += re_real ? 16 : 64;
+                for (int e = 0; e < (re_real ? 16 : 64); ++e) T[e] = 0.0;
+                for (int t : u.terms) {
+                    const int ycnt = __builtin_popcountll(y[t]);
+                    const double sgn = ((ycnt & 3) == 1 || (ycnt & 3) == 2) ? -2.0 : 2.0;
+                    const double fx = sgn * coeffs[2 * t], fy = sgn * coeffs[2 * t + 1];
+                    const int mq = to_reg(to_tile((z[t] | y[t]) & B));
+                    for (int rho = 0; rho < 16; ++rho) {
+                        const int r = ((rho >> H) << (H + 1)) | (rho & ((1 << H) - 1));
+                        const double sg = (__builtin_popcount(static_cast<unsigned>(r & mq)) & 1) ? -1.0 : 1.0;
+                        if (re_real) {
+                            T[rho] += sg * fx;
+                        } else if (ycnt & 1) {
+                            T[32 + rho] += sg * fx;
+                            T[48 + rho] += sg * fy;
+                        } else {
+                            T[rho] += sg * fx;
+                            T[16 + rho] += sg * fy;
+                        }
+                    }
+                }
+            }
+            P->sets[P->n_sets++] = Sc;
+            ++plan.coset_sets;
+            at = end;
+        }
+    }
+    plan.cosets.push_back(std::move(P));
+}
+
+}  // namespace
 
 // Host planning of one EVC tile: flip-mask groups, tile passes, coefficient
 // folding, and the wide (full-vector) groups.  No device access.
@@ -491,12 +758,43 @@ PauliPlanHost build_pauli_plan(int nl, int pe_begin, int n_terms, const std::uin
         if (T == nl) {
             B = local_mask;
         } else {
-            for (int gi : left) {
-                const std::uint64_t m = flips[static_cast<std::size_t>(gi)].first;
-                if (popc(B | m) <= T) B |= m;
-                if (popc(B) == T) break;
+            // candidates: greedy unions of flip masks seeded at each of the
+            // first remaining groups, and windows of consecutive positions
+            // above the coalescing bits (Jordan-Wigner masks are local in
+            // qubit order); the one holding most remaining groups wins
+            auto covered = [&](std::uint64_t b) {
+                int n = 0;
+                for (int gi : left) n += (flips[static_cast<std::size_t>(gi)].first & ~b) == 0;
+                return n;
+            };
+            auto fill = [&](std::uint64_t b) {
+                for (int p = 0; p < nl && popc(b) < T; ++p) b |= 1ull << p;
+                return b;
+            };
+            int best = -1;
+            const std::size_t seeds = std::min<std::size_t>(16, left.size());
+            for (std::size_t sd = 0; sd < std::max<std::size_t>(seeds, 1); ++sd) {
+                std::uint64_t b = (1ull << coal) - 1;
+                for (std::size_t q = 0; q < left.size(); ++q) {
+                    const std::uint64_t m = flips[static_cast<std::size_t>(left[(sd + q) % left.size()])].first;
+                    if (popc(b | m) <= T) b |= m;
+                    if (popc(b) == T) break;
+                }
+                b = fill(b);
+                const int got = covered(b);
+                if (got > best) {
+                    best = got;
+                    B = b;
+                }
             }
-            for (int p = 0; p < nl && popc(B) < T; ++p) B |= 1ull << p;
+            for (int w = coal; w + (T - coal) <= nl; ++w) {
+                const std::uint64_t b = ((1ull << coal) - 1) | (((1ull << (T - coal)) - 1) << w);
+                const int got = covered(b);
+                if (got > best) {
+                    best = got;
+                    B = b;
+                }
+            }
         }
         Pass ps{B, {}, !diag_done};
         diag_done = true;
@@ -509,7 +807,16 @@ PauliPlanHost build_pauli_plan(int nl, int pe_begin, int n_terms, const std::uin
     }
 
     // ---- device descriptors ---------------------------------------------------
+    const bool coset_ok = coset_enabled() && nl >= kTileBits && T == kTileBits;
     for (const Pass& ps : passes) {
+        bool coset = coset_ok;
+        for (int gi : ps.groups)
+            if (popc(flips[static_cast<std::size_t>(gi)].first) > kCosetBits) coset = false;
+        if (coset) {
+            build_coset_pass(plan, nl, pe_begin, ps.B, flips, ps.groups, ps.has_diag ? diag : std::vector<int>{}, y, z,
+                             gz, coeffs);
+            continue;
+        }
         PPass h{};
         h.T = T;
         h.pe_begin = pe_begin;
@@ -637,12 +944,14 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
     const std::size_t gbytes = dgroups.size() * sizeof(PGroup);
     const std::size_t toff = (gbytes + 255) & ~std::size_t{255};
     const std::size_t woff = (toff + dterms.size() * sizeof(PTerm) + 255) & ~std::size_t{255};
-    const std::size_t total = woff + wgroups.size() * sizeof(WGroup) + 16;
+    const std::size_t coff = (woff + wgroups.size() * sizeof(WGroup) + 255) & ~std::size_t{255};
+    const std::size_t total = coff + plan.cdterms.size() * sizeof(CosetDiagTerm) + 16;
     char* host = static_cast<char*>(ensure_pinned(st, total));
     QRT_CUDA(cudaStreamSynchronize(st->stream));
     std::memcpy(host, dgroups.data(), gbytes);
     std::memcpy(host + toff, dterms.data(), dterms.size() * sizeof(PTerm));
     std::memcpy(host + woff, wgroups.data(), wgroups.size() * sizeof(WGroup));
+    std::memcpy(host + coff, plan.cdterms.data(), plan.cdterms.size() * sizeof(CosetDiagTerm));
     char* dev = static_cast<char*>(ensure_ops(st, total));
     QRT_CUDA(cudaMemcpyAsync(dev, host, total, cudaMemcpyHostToDevice, st->stream));
 
@@ -661,6 +970,13 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
     for (int i = 0; i < st->pe_count; ++i) ptrs.p[i] = st->live(i);
     {
         ProfileScope prof(st, QRT_K_PAULI);
+        for (auto& cp : plan.cosets) {
+            for (int i = 0; i < st->pe_count; ++i) cp->ptrs[i] = st->live(i);
+            launch_coset_pass(*cp, reinterpret_cast<const CosetDiagTerm*>(dev + coff), st->pe_count, red, st->stream,
+                              st->device);
+            st->stats[QRT_K_PAULI].launches++;
+            st->stats[QRT_K_PAULI].bytes += 16.0 * static_cast<double>(st->amps) * st->pe_count;
+        }
         for (const PPass& h : hdrs) {
             const std::size_t smem = (std::size_t{1} << T) * sizeof(double2) +
                                      (std::size_t{1} << (T - h.c)) * sizeof(std::uint64_t) +
@@ -697,8 +1013,14 @@ void pauli_plan_info(int nl, int n_terms, const std::uint64_t* x, const std::uin
     const auto t0 = std::chrono::steady_clock::now();
     PauliPlanHost plan = build_pauli_plan(nl, 0, n_terms, x, y, z, gz, coeffs);
     const auto t1 = std::chrono::steady_clock::now();
-    if (passes) *passes = static_cast<int>(plan.hdrs.size());
-    if (groups) *groups = static_cast<int>(plan.dgroups.size());
+    if (std::getenv("QRT_DEBUG_PLAN"))
+        std::fprintf(stderr, "evc plan: %zu tiled passes, %zu coset launches, %d coset sets, %zu wide groups\n",
+                     plan.hdrs.size(), plan.cosets.size(), plan.coset_sets, plan.wgroups.size());
+    if (passes) *passes = static_cast<int>(plan.hdrs.size() + plan.cosets.size());
+    int coset_groups = 0;
+    for (const auto& cp : plan.cosets)
+        for (int si = 0; si < cp->n_sets; ++si) coset_groups += cp->sets[si].g_count;
+    if (groups) *groups = static_cast<int>(plan.dgroups.size()) + coset_groups;
     if (wide_groups) *wide_groups = static_cast<int>(plan.wgroups.size());
     if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
 }

@@ -5,6 +5,8 @@
 // evaluated pair-wise over the canonical half of each flip-mask group.
 // One CTA = one 2^12-amplitude tile = 128 threads x 32-amplitude cosets.
 
+#include <cstdlib>
+
 #include "qrt_coset.h"
 
 namespace qrt {
@@ -29,15 +31,20 @@ __host__ __device__ constexpr int ins0(int v, int bit) { return ((v >> bit) << (
 // (r, r^XQ) of the coset, r without the top bit of XQ (register indices are
 // compile-time: one code body per mask).
 template <int XQ>
-__device__ __forceinline__ double coset_group(const double2 (&a)[32], const double* __restrict__ T) {
+__device__ __forceinline__ double coset_group(const double2 (&a)[32], const double2* __restrict__ T2) {
     constexpr int H = top_bit(XQ);
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int rho = 0; rho < 16; ++rho) {
-        const int r = ins0(rho, H);
-        const int s = r ^ XQ;
-        const double2 A = a[s], B = a[r];
-        acc[rho & 3] = fma(T[rho], fma(A.x, B.x, A.y * B.y), acc[rho & 3]);
+    for (int h = 0; h < 8; ++h) {
+        const double2 t = T2[h];  // table entries 2h, 2h+1 (shared-memory broadcast)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int rho = 2 * h + u;
+            const int r = ins0(rho, H);
+            const int s = r ^ XQ;
+            const double2 A = a[s], B = a[r];
+            acc[rho & 3] = fma(u ? t.y : t.x, fma(A.x, B.x, A.y * B.y), acc[rho & 3]);
+        }
     }
     return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
@@ -76,11 +83,12 @@ __device__ __noinline__ double2 coset_generic(const double2* __restrict__ tile, 
 // mask, no switch), so the coset stays in registers.
 template <int XQ>
 __device__ __forceinline__ void coset_fast(const double2 (&a)[32], const CosetParams& P, const CosetSet& S,
-                                           std::uint64_t W, std::uint64_t pe, double2& acc) {
+                                           const double2* __restrict__ tabs, std::uint64_t W, std::uint64_t pe,
+                                           double2& acc) {
     const int g0 = S.g_begin + S.xbeg[XQ - 1], g1 = S.g_begin + S.xbeg[XQ];
     for (int g = g0; g < g1; ++g) {
         const CosetGroup& G = P.groups[g];
-        const double r = coset_group<XQ>(a, P.tabs + G.tab);
+        const double r = coset_group<XQ>(a, tabs + (G.tab >> 1));
         const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
         acc.x += odd ? -r : r;
     }
@@ -105,7 +113,8 @@ __device__ __forceinline__ double2 block_sum(double2 v, double2* scratch) {
     return r;
 }
 
-__global__ void __launch_bounds__(kCosetThreads, 2)
+template <int MINB>
+__global__ void __launch_bounds__(kCosetThreads, MINB)
     coset_pass_kernel(const __grid_constant__ CosetParams P, const CosetDiagTerm* __restrict__ dterms,
                       double* __restrict__ red) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -114,7 +123,10 @@ __global__ void __launch_bounds__(kCosetThreads, 2)
     const int c = P.c, t = threadIdx.x;
     double2* tile = reinterpret_cast<double2*>(smem_raw);
     u64* tabo = reinterpret_cast<u64*>(tile + E);
-    double* Wsh = reinterpret_cast<double*>(tabo + (1 << (kTileBits - c)));
+    double2* stab = reinterpret_cast<double2*>(tabo + ((1 << (kTileBits - c)) | 1) + 1);  // 16-B aligned tables
+    double* Wsh = reinterpret_cast<double*>(stab + (P.n_tab >> 1));
+    for (int i = t; i < (P.n_tab >> 1); i += kCosetThreads)
+        stab[i] = make_double2(P.tabs[2 * i], P.tabs[2 * i + 1]);
 
     const u64 b = static_cast<u64>(blockIdx.x);  // bit i <-> outer_pos[i]
     u64 base = 0;
@@ -180,21 +192,21 @@ __global__ void __launch_bounds__(kCosetThreads, 2)
             a[r] = tile[o];
         }
         const u64 W = static_cast<u64>(ebase) | wout;
-        coset_fast<3>(a, P, S, W, pe, acc);
-        coset_fast<5>(a, P, S, W, pe, acc);
-        coset_fast<6>(a, P, S, W, pe, acc);
-        coset_fast<9>(a, P, S, W, pe, acc);
-        coset_fast<10>(a, P, S, W, pe, acc);
-        coset_fast<12>(a, P, S, W, pe, acc);
-        coset_fast<15>(a, P, S, W, pe, acc);
-        coset_fast<17>(a, P, S, W, pe, acc);
-        coset_fast<18>(a, P, S, W, pe, acc);
-        coset_fast<20>(a, P, S, W, pe, acc);
-        coset_fast<23>(a, P, S, W, pe, acc);
-        coset_fast<24>(a, P, S, W, pe, acc);
-        coset_fast<27>(a, P, S, W, pe, acc);
-        coset_fast<29>(a, P, S, W, pe, acc);
-        coset_fast<30>(a, P, S, W, pe, acc);
+        coset_fast<3>(a, P, S, stab, W, pe, acc);
+        coset_fast<5>(a, P, S, stab, W, pe, acc);
+        coset_fast<6>(a, P, S, stab, W, pe, acc);
+        coset_fast<9>(a, P, S, stab, W, pe, acc);
+        coset_fast<10>(a, P, S, stab, W, pe, acc);
+        coset_fast<12>(a, P, S, stab, W, pe, acc);
+        coset_fast<15>(a, P, S, stab, W, pe, acc);
+        coset_fast<17>(a, P, S, stab, W, pe, acc);
+        coset_fast<18>(a, P, S, stab, W, pe, acc);
+        coset_fast<20>(a, P, S, stab, W, pe, acc);
+        coset_fast<23>(a, P, S, stab, W, pe, acc);
+        coset_fast<24>(a, P, S, stab, W, pe, acc);
+        coset_fast<27>(a, P, S, stab, W, pe, acc);
+        coset_fast<29>(a, P, S, stab, W, pe, acc);
+        coset_fast<30>(a, P, S, stab, W, pe, acc);
         for (int g = S.g_begin + S.xbeg[31]; g < S.g_begin + S.g_count; ++g) {
             const CosetGroup& G = P.groups[g];
             const double2 r = coset_generic(tile, sb, swq, G.xq, G.mode, P.tabs + G.tab);
@@ -215,16 +227,26 @@ __global__ void __launch_bounds__(kCosetThreads, 2)
 
 void launch_coset_pass(const CosetParams& P, const CosetDiagTerm* dterms, int pe_count, double* red,
                        cudaStream_t stream, int device) {
+    // default 2 CTAs/SM without spills; QRT_COSET_OCC=3: 3 CTAs/SM (168 registers, spills)
+    static const int occ = [] {
+        const char* e = std::getenv("QRT_COSET_OCC");
+        return (e && std::atoi(e) == 3) ? 3 : 2;
+    }();
     static bool attr_done[64] = {};
     if (!attr_done[device]) {
-        QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
+        QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
+        QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
         attr_done[device] = true;
     }
     const std::size_t smem = (std::size_t{1} << kTileBits) * sizeof(double2) +
-                             (std::size_t{1} << (kTileBits - P.c)) * sizeof(std::uint64_t) +
+                             ((std::size_t{1} << (kTileBits - P.c)) + 2) * sizeof(std::uint64_t) +
+                             static_cast<std::size_t>(P.n_tab) * sizeof(double) +
                              (P.d_count > 0 ? (std::size_t{1} << kTileBits) * sizeof(double) : 0);
     dim3 grid(static_cast<unsigned>(P.tiles_per_pe), static_cast<unsigned>(pe_count));
-    coset_pass_kernel<<<grid, kCosetThreads, smem, stream>>>(P, dterms, red);
+    if (occ == 2)
+        coset_pass_kernel<2><<<grid, kCosetThreads, smem, stream>>>(P, dterms, red);
+    else
+        coset_pass_kernel<3><<<grid, kCosetThreads, smem, stream>>>(P, dterms, red);
     QRT_CUDA(cudaGetLastError());
 }
 

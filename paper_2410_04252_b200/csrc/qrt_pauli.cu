@@ -704,6 +704,7 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
                 }
             }
             P->sets[P->n_sets++] = Sc;
+            P->n_tab = n_tab;
             ++plan.coset_sets;
             at = end;
         }

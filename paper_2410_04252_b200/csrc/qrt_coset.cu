@@ -125,8 +125,10 @@ __global__ void __launch_bounds__(kCosetThreads, MINB)
     u64* tabo = reinterpret_cast<u64*>(tile + E);
     double2* stab = reinterpret_cast<double2*>(tabo + ((1 << (kTileBits - c)) | 1) + 1);  // 16-B aligned tables
     double* Wsh = reinterpret_cast<double*>(stab + (P.n_tab >> 1));
-    for (int i = t; i < (P.n_tab >> 1); i += kCosetThreads)
-        stab[i] = make_double2(P.tabs[2 * i], P.tabs[2 * i + 1]);
+    for (int i = t; i < (P.n_tab >> 1); i += kCosetThreads) {
+        const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&stab[i]));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(P.gtabs + 2 * i));
+    }
 
     const u64 b = static_cast<u64>(blockIdx.x);  // bit i <-> outer_pos[i]
     u64 base = 0;

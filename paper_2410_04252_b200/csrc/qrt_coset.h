@@ -54,6 +54,7 @@ struct CosetParams {
     int tiles_per_pe;
     int d_begin, d_count;  // I/Z words of this pass (global term array), Walsh-Hadamard path
     int n_tab;             // doubles of tabs in use (staged in shared memory)
+    const double* gtabs;   // device copy of tabs[0, n_tab) (coalesced staging)
     std::int8_t tile_pos[kTileBits];
     std::int8_t outer_pos[64];
     CosetSet sets[kCosetMaxSets];

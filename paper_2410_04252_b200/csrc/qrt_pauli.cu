@@ -946,13 +946,22 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
     const std::size_t toff = (gbytes + 255) & ~std::size_t{255};
     const std::size_t woff = (toff + dterms.size() * sizeof(PTerm) + 255) & ~std::size_t{255};
     const std::size_t coff = (woff + wgroups.size() * sizeof(WGroup) + 255) & ~std::size_t{255};
-    const std::size_t total = coff + plan.cdterms.size() * sizeof(CosetDiagTerm) + 16;
+    const std::size_t goff = (coff + plan.cdterms.size() * sizeof(CosetDiagTerm) + 255) & ~std::size_t{255};
+    std::vector<std::size_t> tab_off;
+    std::size_t gend = goff;
+    for (const auto& cp : plan.cosets) {
+        tab_off.push_back(gend);
+        gend = (gend + static_cast<std::size_t>(cp->n_tab) * sizeof(double) + 255) & ~std::size_t{255};
+    }
+    const std::size_t total = gend + 16;
     char* host = static_cast<char*>(ensure_pinned(st, total));
     QRT_CUDA(cudaStreamSynchronize(st->stream));
     std::memcpy(host, dgroups.data(), gbytes);
     std::memcpy(host + toff, dterms.data(), dterms.size() * sizeof(PTerm));
     std::memcpy(host + woff, wgroups.data(), wgroups.size() * sizeof(WGroup));
     std::memcpy(host + coff, plan.cdterms.data(), plan.cdterms.size() * sizeof(CosetDiagTerm));
+    for (std::size_t i = 0; i < plan.cosets.size(); ++i)
+        std::memcpy(host + tab_off[i], plan.cosets[i]->tabs, static_cast<std::size_t>(plan.cosets[i]->n_tab) * sizeof(double));
     char* dev = static_cast<char*>(ensure_ops(st, total));
     QRT_CUDA(cudaMemcpyAsync(dev, host, total, cudaMemcpyHostToDevice, st->stream));
 
@@ -971,7 +980,9 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
     for (int i = 0; i < st->pe_count; ++i) ptrs.p[i] = st->live(i);
     {
         ProfileScope prof(st, QRT_K_PAULI);
-        for (auto& cp : plan.cosets) {
+        for (std::size_t ci = 0; ci < plan.cosets.size(); ++ci) {
+            auto& cp = plan.cosets[ci];
+            cp->gtabs = reinterpret_cast<const double*>(dev + tab_off[ci]);
             for (int i = 0; i < st->pe_count; ++i) cp->ptrs[i] = st->live(i);
             launch_coset_pass(*cp, reinterpret_cast<const CosetDiagTerm*>(dev + coff), st->pe_count, red, st->stream,
                               st->device);

@@ -292,20 +292,47 @@ def run_ours(args):
     st, _, _, _, _ = step(profile=True)
     stats = st.stats()
     del st
-    g = stats["gates"]
-    gate_ms = g["ms"] / max(1, g["launches"])
-    gate_bytes = g["bytes"] / max(1, g["launches"])
-    achieved = gate_bytes / (gate_ms / 1e3) / 1e9 if gate_ms > 0 else None
-    fp64 = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else None
-    qr = stats["qr"]
-    pa = stats["pauli"]
-    traffic = None
-    try:  # DRAM bytes per gate-pass launch from the committed `ncu --set full` capture
+    g, qr, pa = stats["gates"], stats["qr"], stats["pauli"]
+    fam_kernel = {"gates": ("gate_pass_kernel (DMMA fp64 tensor, dense 3/4-qubit gates)" if args.circuit == "gatefabric"
+                            else "light_pass_kernel (register-resident 1q/2q/diagonal runs)"),
+                  "pauli": "coset_pass_kernel (EVC, 5-qubit register cosets)"}
+    try:  # DRAM bytes per launch from the committed `ncu --set full` captures (same n, p, circuit)
         tr = json.loads((ROOT / "profiles" / "roofline_traffic.json").read_text())
-        if tr.get("qubits") == n and tr.get("pes") == p:
-            traffic = tr["gate_pass_kernel"]["dram_bytes_per_launch"]
     except Exception:
-        traffic = None
+        tr = {}
+
+    def family(name, st, bytes_unit):
+        """Achieved vs peak for one kernel family from the profiled step's CUDA events.
+        bytes: algorithmic HBM bytes (gates: 32 B x amplitudes per pass, EVC: 16 B per pass);
+        flops: reference-equivalent fp64 flops (8*2^k per amplitude per dense k-qubit gate,
+        8 per amplitude per Pauli string)."""
+        if st["launches"] == 0 or st["ms"] <= 0:
+            return None
+        sec = st["ms"] / 1e3
+        gbs = st["bytes"] / sec / 1e9
+        tf = st["flops"] / sec / 1e12
+        key = f"{args.circuit}:{name}:{n}:{p}"
+        traffic = tr.get(key, {}).get("dram_bytes_per_launch")
+        return {"kernel": fam_kernel.get(name, name), "ms": st["ms"], "launches": st["launches"],
+                "avg_launch_ms": st["ms"] / st["launches"], "algorithmic_bytes_per_launch": st["bytes"] / st["launches"],
+                "algorithmic_flops_per_launch": st["flops"] / st["launches"], "hbm_gbs": gbs,
+                "hbm_frac": gbs / hbm_peak, "fp64_tflops_ref_equiv": tf, "fp64_frac": tf / FP64_TENSOR_PEAK,
+                "traffic": traffic}
+
+    fams = {k: v for k, v in (("gates", family("gates", g, 32)), ("pauli", family("pauli", pa, 16))) if v}
+    top = max(fams, key=lambda k: fams[k]["ms"])
+    f = fams[top]
+    if top == "gates" and args.circuit == "gatefabric":
+        # dense 4-qubit blocks on the fp64 tensor pipe: flop-bound (SURVEY.md section 7 hard parts)
+        roof = {"bound": "tensor", "achieved": f["fp64_tflops_ref_equiv"], "peak": FP64_TENSOR_PEAK, "unit": "TFLOP/s",
+                "frac": f["fp64_frac"], "peak_kind": "measured fp64 DMMA (tools/microbench_fp64.cu)"}
+    else:
+        # light passes and EVC passes: one HBM round trip (gates) / read (EVC) per pass
+        roof = {"bound": "hbm", "achieved": f["hbm_gbs"], "peak": hbm_peak, "unit": "GB/s", "frac": f["hbm_frac"],
+                "peak_kind": peak_kind}
+    roof.update({"kernel": f["kernel"], "traffic": f["traffic"], "avg_launch_ms": f["avg_launch_ms"],
+                 "algorithmic_bytes_per_launch": f["algorithmic_bytes_per_launch"],
+                 "algorithmic_flops_per_launch": f["algorithmic_flops_per_launch"], "families": fams})
     mat_bytes = sum(16 * (1 << (2 * op.arity())) for op in circuit.operators)
     term_bytes = 8 * 5 * n_terms
     d2h = 16 * p * max(1, len(plan.tiles))
@@ -320,14 +347,7 @@ def run_ours(args):
         "e2e": {"value": wall_t, "unit": "s", "h2d_bytes_per_step": mat_bytes + term_bytes, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches // max(1, args.steps),
         "clocks": clk,
-        "roofline": {"bound": "tensor", "kernel": "gate_pass_kernel (QSU; DMMA fp64 tensor path)",
-                     "achieved": fp64, "peak": FP64_TENSOR_PEAK, "unit": "TFLOP/s",
-                     "frac": (fp64 / FP64_TENSOR_PEAK) if fp64 else None, "traffic": traffic,
-                     "peak_kind": "measured fp64 DMMA (tools/microbench_fp64.cu)",
-                     "avg_launch_ms": gate_ms, "algorithmic_bytes_per_launch": gate_bytes,
-                     "algorithmic_flops_per_launch": g["flops"] / max(1, g["launches"]),
-                     "hbm": {"achieved_gbs": achieved, "peak_gbs": hbm_peak, "peak_kind": peak_kind,
-                             "frac": (achieved / hbm_peak) if achieved else None}},
+        "roofline": roof,
         "phases_ms": {"gates": g["ms"], "qr": qr["ms"], "pauli": pa["ms"], "misc": stats["misc"]["ms"],
                       "gate_passes": g["launches"], "qr_launches": qr["launches"], "pauli_passes": pa["launches"],
                       "qr_nvlink_gbs": (qr["bytes"] / (qr["ms"] / 1e3) / 1e9) if qr["ms"] > 0 else None},

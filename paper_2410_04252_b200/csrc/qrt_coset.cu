@@ -24,6 +24,7 @@ __device__ __forceinline__ int insert_zero(int v, int bit) {
     return ((v >> bit) << (bit + 1)) | (v & ((1 << bit) - 1));
 }
 
+__host__ __device__ constexpr int ctz_c(int v) { return (v & 1) ? 0 : (v & 2) ? 1 : (v & 4) ? 2 : (v & 8) ? 3 : 4; }
 __host__ __device__ constexpr int top_bit(int v) { return v >= 16 ? 4 : v >= 8 ? 3 : v >= 4 ? 2 : v >= 2 ? 1 : 0; }
 __host__ __device__ constexpr int ins0(int v, int bit) { return ((v >> bit) << (bit + 1)) | (v & ((1 << bit) - 1)); }
 
@@ -83,8 +84,9 @@ __device__ __noinline__ double2 coset_generic(const double2* __restrict__ tile, 
 // mask, no switch), so the coset stays in registers.
 template <int XQ>
 __device__ __forceinline__ void coset_fast(const double2 (&a)[32], const CosetParams& P, const CosetSet& S,
-                                           const double2* __restrict__ tabs, std::uint64_t W, std::uint64_t pe,
-                                           double2& acc) {
+                                           const double2* __restrict__ tabs, unsigned present, std::uint64_t W,
+                                           std::uint64_t pe, double2& acc) {
+    if (!((present >> XQ) & 1u)) return;
     const int g0 = S.g_begin + S.xbeg[XQ - 1], g1 = S.g_begin + S.xbeg[XQ];
     for (int g = g0; g < g1; ++g) {
         const CosetGroup& G = P.groups[g];
@@ -113,7 +115,7 @@ __device__ __forceinline__ double2 block_sum(double2 v, double2* scratch) {
     return r;
 }
 
-template <int MINB>
+template <int MINB, bool GRAY>
 __global__ void __launch_bounds__(kCosetThreads, MINB)
     coset_pass_kernel(const __grid_constant__ CosetParams P, const CosetDiagTerm* __restrict__ dterms,
                       double* __restrict__ red) {
@@ -185,30 +187,42 @@ __global__ void __launch_bounds__(kCosetThreads, MINB)
         for (int q = 0; q < kCosetBits; ++q) swq[q] = swz(1 << S.S[q]);
         const int sb = swz(ebase);
         double2 a[32];
-#pragma unroll
-        for (int r = 0; r < 32; ++r) {
+        if (GRAY) {
+            // Gray-code walk over the coset: one XOR per amplitude address
             int o = sb;
 #pragma unroll
-            for (int q = 0; q < kCosetBits; ++q)
-                if ((r >> q) & 1) o ^= swq[q];
-            a[r] = tile[o];
+            for (int i = 0; i < 32; ++i) {
+                const int r = i ^ (i >> 1);
+                a[r] = tile[o];
+                if (i < 31) o ^= swq[ctz_c(i + 1)];
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+                int o = sb;
+#pragma unroll
+                for (int q = 0; q < kCosetBits; ++q)
+                    if ((r >> q) & 1) o ^= swq[q];
+                a[r] = tile[o];
+            }
         }
         const u64 W = static_cast<u64>(ebase) | wout;
-        coset_fast<3>(a, P, S, stab, W, pe, acc);
-        coset_fast<5>(a, P, S, stab, W, pe, acc);
-        coset_fast<6>(a, P, S, stab, W, pe, acc);
-        coset_fast<9>(a, P, S, stab, W, pe, acc);
-        coset_fast<10>(a, P, S, stab, W, pe, acc);
-        coset_fast<12>(a, P, S, stab, W, pe, acc);
-        coset_fast<15>(a, P, S, stab, W, pe, acc);
-        coset_fast<17>(a, P, S, stab, W, pe, acc);
-        coset_fast<18>(a, P, S, stab, W, pe, acc);
-        coset_fast<20>(a, P, S, stab, W, pe, acc);
-        coset_fast<23>(a, P, S, stab, W, pe, acc);
-        coset_fast<24>(a, P, S, stab, W, pe, acc);
-        coset_fast<27>(a, P, S, stab, W, pe, acc);
-        coset_fast<29>(a, P, S, stab, W, pe, acc);
-        coset_fast<30>(a, P, S, stab, W, pe, acc);
+        const unsigned present = S.present;
+        coset_fast<3>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<5>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<6>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<9>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<10>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<12>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<15>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<17>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<18>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<20>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<23>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<24>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<27>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<29>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<30>(a, P, S, stab, present, W, pe, acc);
         for (int g = S.g_begin + S.xbeg[31]; g < S.g_begin + S.g_count; ++g) {
             const CosetGroup& G = P.groups[g];
             const double2 r = coset_generic(tile, sb, swq, G.xq, G.mode, P.tabs + G.tab);
@@ -229,15 +243,15 @@ __global__ void __launch_bounds__(kCosetThreads, MINB)
 
 void launch_coset_pass(const CosetParams& P, const CosetDiagTerm* dterms, int pe_count, double* red,
                        cudaStream_t stream, int device) {
-    // default 2 CTAs/SM without spills; QRT_COSET_OCC=3: 3 CTAs/SM (168 registers, spills)
-    static const int occ = [] {
-        const char* e = std::getenv("QRT_COSET_OCC");
-        return (e && std::atoi(e) == 3) ? 3 : 2;
+    // 2 CTAs/SM without spills; QRT_COSET_GRAY=1 loads the coset along a Gray code
+    static const bool gray = [] {
+        const char* e = std::getenv("QRT_COSET_GRAY");
+        return e && std::atoi(e) != 0;
     }();
     static bool attr_done[64] = {};
     if (!attr_done[device]) {
-        QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
-        QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
+        QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
+        QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
         attr_done[device] = true;
     }
     const std::size_t smem = (std::size_t{1} << kTileBits) * sizeof(double2) +
@@ -245,10 +259,10 @@ void launch_coset_pass(const CosetParams& P, const CosetDiagTerm* dterms, int pe
                              static_cast<std::size_t>(P.n_tab) * sizeof(double) +
                              (P.d_count > 0 ? (std::size_t{1} << kTileBits) * sizeof(double) : 0);
     dim3 grid(static_cast<unsigned>(P.tiles_per_pe), static_cast<unsigned>(pe_count));
-    if (occ == 2)
-        coset_pass_kernel<2><<<grid, kCosetThreads, smem, stream>>>(P, dterms, red);
+    if (gray)
+        coset_pass_kernel<2, true><<<grid, kCosetThreads, smem, stream>>>(P, dterms, red);
     else
-        coset_pass_kernel<3><<<grid, kCosetThreads, smem, stream>>>(P, dterms, red);
+        coset_pass_kernel<2, false><<<grid, kCosetThreads, smem, stream>>>(P, dterms, red);
     QRT_CUDA(cudaGetLastError());
 }
 

@@ -41,6 +41,7 @@ struct CosetSet {
     std::int8_t S[kCosetBits];                // tile bit of register bit q
     std::int8_t tb[kTileBits - kCosetBits];   // tile bit of thread-index bit i
     std::int16_t g_begin, g_count;
+    std::uint32_t present;  // bit x: some fast group has mask x
     std::uint8_t xbeg[32];  // fast groups sorted by mask: [xbeg[x-1], xbeg[x]) have mask x; generic from xbeg[31]
 };
 

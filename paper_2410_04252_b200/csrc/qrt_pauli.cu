@@ -670,6 +670,9 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
                 for (std::size_t q = at; q < end; ++q) cnt += fast_of(subs[q]) && subs[q].xq <= xq;
                 Sc.xbeg[xq] = static_cast<std::uint8_t>(cnt);  // fast subgroups with mask <= xq
             }
+            Sc.present = 0;
+            for (std::size_t q = at; q < end; ++q)
+                if (fast_of(subs[q])) Sc.present |= 1u << subs[q].xq;
             for (std::size_t q = at; q < end; ++q) {
                 const Sub& u = subs[q];
                 CosetGroup& G = P->groups[n_groups++];

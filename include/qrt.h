@@ -125,6 +125,13 @@ qrt_status qrt_pauli_plan_info(int n_local, int n_terms, const uint64_t* x, cons
                                const uint64_t* gz, const double* coeffs, int* passes, int* groups, int* wide_groups,
                                double* seconds);
 
+/* Host-only: the pass plan qrt_apply_gates would build for these gates on a
+ * PE of n_local positions: HBM passes, light (register-resident) passes and
+ * their register stages, and 1-qubit gates fused into a neighbour on the
+ * host.  No device needed. */
+qrt_status qrt_gate_plan_info(int n_local, int n_gates, const int* arity, const int* pos, const double* mats,
+                              const unsigned* flags, int* passes, int* light_passes, int* light_stages, int* fused);
+
 /* sqrt(sum |amp|^2) over all PEs (DistributedState::norm, dist_sim.cpp:115). */
 qrt_status qrt_norm(qrt_state* st, double* out);
 

@@ -531,6 +531,14 @@ qrt_status qrt_pauli_plan_info(int n_local, int n_terms, const std::uint64_t* x,
     });
 }
 
+qrt_status qrt_gate_plan_info(int n_local, int n_gates, const int* arity, const int* pos, const double* mats,
+                              const unsigned* flags, int* passes, int* light_passes, int* light_stages, int* fused) {
+    return guarded([&] {
+        require(n_gates >= 0 && (n_gates == 0 || (arity && pos && mats)), QRT_ERR_INVALID, "null gate arrays");
+        gate_plan_info(n_local, n_gates, arity, pos, mats, flags, passes, light_passes, light_stages, fused);
+    });
+}
+
 qrt_status qrt_norm(qrt_state* st, double* out) {
     TraceScope trace_("qrt_norm");
     return guarded([&] {

@@ -596,16 +596,29 @@ int plan_light_stages(const std::vector<HostOp>& opsv, const std::vector<int>& t
     return applied;
 }
 
-}  // namespace
 
-void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, const double* mats,
-                 const unsigned* flags) {
-    const int nl = st->nl;
-    const double amps_all = static_cast<double>(st->amps) * st->pe_count;
+constexpr int kLightMarker = 1 << 20;  // PassHdr::T of a light pass: marker + index into GatePlan::light
+
+// The device program of one qrt_apply_gates call, built on the host.
+struct GatePlan {
+    std::vector<GateOp> dev_ops;
+    std::vector<PassHdr> hdrs;  // one per pass (T >= kLightMarker: light pass, T < 0: wide gate)
+    std::vector<double2> pool;
+    std::vector<std::vector<double2>> pmats;
+    std::vector<double> frags;
+    std::vector<int> wide_pos;
+    std::vector<std::unique_ptr<LightParams>> light;
+    double flops_per_amp = 0.0;  // reference-equivalent flops of the gates as given
+    int fused = 0;               // 1-qubit gates folded into a neighbour
+};
+
+GatePlan plan_gates(int nl, int n_gates, const int* arity, const int* pos, const double* mats, const unsigned* flags) {
+    GatePlan plan;
+    const double amps_all = 1.0;  // flops are accumulated per amplitude
     // ---- decode and validate -------------------------------------------------
     std::vector<HostOp> opsv(static_cast<std::size_t>(n_gates));
     std::size_t pcur = 0, mcur = 0;
-    double call_flops = 0.0;  // reference-equivalent flops of the gates as given
+    double& call_flops = plan.flops_per_amp;
     for (int i = 0; i < n_gates; ++i) {
         HostOp& h = opsv[static_cast<std::size_t>(i)];
         h.k = arity[i];
@@ -684,6 +697,7 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
             fused.push_back(r);
             b.m = fused.back().data();
             dead[static_cast<std::size_t>(i)] = 1;
+            ++plan.fused;
         }
     }
     for (HostOp& h : opsv) {
@@ -864,14 +878,14 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
     }
 
     // ---- pack descriptors + matrices into one upload ------------------------------
-    std::vector<GateOp> dev_ops;
-    std::vector<PassHdr> hdrs;
-    std::vector<double2> pool;
-    std::vector<std::vector<double2>> pmats(passes.size());
-    std::vector<double> frags;
-    std::vector<int> wide_pos;  // for wide passes: positions (kBigK per pass)
-    std::vector<std::unique_ptr<LightParams>> light;
-    constexpr int kLightMarker = 1 << 20;  // PassHdr::T of a light pass: marker + index into `light`
+    std::vector<GateOp>& dev_ops = plan.dev_ops;
+    std::vector<PassHdr>& hdrs = plan.hdrs;
+    std::vector<double2>& pool = plan.pool;
+    std::vector<std::vector<double2>>& pmats = plan.pmats;
+    pmats.resize(passes.size());
+    std::vector<double>& frags = plan.frags;
+    std::vector<int>& wide_pos = plan.wide_pos;  // for wide passes: positions (kBigK per pass)
+    std::vector<std::unique_ptr<LightParams>>& light = plan.light;
     auto build_light = [&](const std::vector<int>& tile_pos, int c, const std::vector<LightStagePlan>& stages) {
         auto L = std::make_unique<LightParams>();
         std::memset(L.get(), 0, sizeof(LightParams));
@@ -1121,7 +1135,23 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
         }
         hdrs.push_back(h);
     }
+    return plan;
+}
 
+}  // namespace
+
+void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, const double* mats,
+                 const unsigned* flags) {
+    GatePlan plan = plan_gates(st->nl, n_gates, arity, pos, mats, flags);
+    const double amps_all = static_cast<double>(st->amps) * st->pe_count;
+    const double call_flops = plan.flops_per_amp * amps_all;
+    const auto& dev_ops = plan.dev_ops;
+    const auto& hdrs = plan.hdrs;
+    const auto& pool = plan.pool;
+    const auto& pmats = plan.pmats;
+    const auto& frags = plan.frags;
+    const auto& wide_pos = plan.wide_pos;
+    auto& light = plan.light;
     const std::size_t ops_bytes = dev_ops.size() * sizeof(GateOp);
     const std::size_t pool_off = (ops_bytes + 255) & ~std::size_t{255};
     const std::size_t pool_bytes = pool.size() * sizeof(double2);
@@ -1190,6 +1220,21 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
         st->stats[QRT_K_GATES].launches++;
         st->stats[QRT_K_GATES].bytes += 32.0 * amps_all;
     }
+}
+
+void gate_plan_info(int nl, int n_gates, const int* arity, const int* pos, const double* mats, const unsigned* flags,
+                    int* passes, int* light_passes, int* light_stages, int* fused) {
+    if (nl < 1 || nl > 62) fail(QRT_ERR_INVALID, "n_local out of range");
+    GatePlan plan = plan_gates(nl, n_gates, arity, pos, mats, flags);
+    int lp = 0, ls = 0;
+    for (const auto& L : plan.light) {
+        ++lp;
+        ls += L->n_stages;
+    }
+    if (passes) *passes = static_cast<int>(plan.hdrs.size());
+    if (light_passes) *light_passes = lp;
+    if (light_stages) *light_stages = ls;
+    if (fused) *fused = plan.fused;
 }
 
 }  // namespace qrt

@@ -111,6 +111,8 @@ void reorder_plan(int n, int p, const int* dest, int src_pe, std::uint64_t* dst_
 void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const std::uint64_t* y,
                        const std::uint64_t* z, const std::uint64_t* gz, const double* coeffs, double* partial);
 double norm(qrt_state* st);
+void gate_plan_info(int nl, int n_gates, const int* arity, const int* pos, const double* mats, const unsigned* flags,
+                    int* passes, int* light_passes, int* light_stages, int* fused);
 void pauli_plan_info(int nl, int n_terms, const std::uint64_t* x, const std::uint64_t* y, const std::uint64_t* z,
                      const std::uint64_t* gz, const double* coeffs, int* passes, int* groups, int* wide_groups,
                      double* seconds);

@@ -24,7 +24,6 @@ __device__ __forceinline__ int insert_zero(int v, int bit) {
     return ((v >> bit) << (bit + 1)) | (v & ((1 << bit) - 1));
 }
 
-__host__ __device__ constexpr int ctz_c(int v) { return (v & 1) ? 0 : (v & 2) ? 1 : (v & 4) ? 2 : (v & 8) ? 3 : 4; }
 __host__ __device__ constexpr int top_bit(int v) { return v >= 16 ? 4 : v >= 8 ? 3 : v >= 4 ? 2 : v >= 2 ? 1 : 0; }
 __host__ __device__ constexpr int ins0(int v, int bit) { return ((v >> bit) << (bit + 1)) | (v & ((1 << bit) - 1)); }
 
@@ -115,7 +114,7 @@ __device__ __forceinline__ double2 block_sum(double2 v, double2* scratch) {
     return r;
 }
 
-template <int MINB, bool GRAY>
+template <int MINB, bool GENERIC>
 __global__ void __launch_bounds__(kCosetThreads, MINB)
     coset_pass_kernel(const __grid_constant__ CosetParams P, const CosetDiagTerm* __restrict__ dterms,
                       double* __restrict__ red) {
@@ -187,16 +186,7 @@ __global__ void __launch_bounds__(kCosetThreads, MINB)
         for (int q = 0; q < kCosetBits; ++q) swq[q] = swz(1 << S.S[q]);
         const int sb = swz(ebase);
         double2 a[32];
-        if (GRAY) {
-            // Gray-code walk over the coset: one XOR per amplitude address
-            int o = sb;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int r = i ^ (i >> 1);
-                a[r] = tile[o];
-                if (i < 31) o ^= swq[ctz_c(i + 1)];
-            }
-        } else {
+        {
 #pragma unroll
             for (int r = 0; r < 32; ++r) {
                 int o = sb;
@@ -223,6 +213,7 @@ __global__ void __launch_bounds__(kCosetThreads, MINB)
         coset_fast<27>(a, P, S, stab, present, W, pe, acc);
         coset_fast<29>(a, P, S, stab, present, W, pe, acc);
         coset_fast<30>(a, P, S, stab, present, W, pe, acc);
+        if (GENERIC)
         for (int g = S.g_begin + S.xbeg[31]; g < S.g_begin + S.g_count; ++g) {
             const CosetGroup& G = P.groups[g];
             const double2 r = coset_generic(tile, sb, swq, G.xq, G.mode, P.tabs + G.tab);
@@ -243,15 +234,21 @@ __global__ void __launch_bounds__(kCosetThreads, MINB)
 
 void launch_coset_pass(const CosetParams& P, const CosetDiagTerm* dterms, int pe_count, double* red,
                        cudaStream_t stream, int device) {
-    // 2 CTAs/SM without spills; QRT_COSET_GRAY=1 loads the coset along a Gray code
-    static const bool gray = [] {
-        const char* e = std::getenv("QRT_COSET_GRAY");
-        return e && std::atoi(e) != 0;
+    // Launches holding only Jordan-Wigner-type groups take the fast-only
+    // kernel (218 registers, 2 CTAs/SM; QRT_COSET_OCC=3 squeezes it to 3 CTAs/SM
+    // with spills, measured slower); any generic group needs the
+    // shared-memory fallback body.
+    static const int occ = [] {
+        const char* e = std::getenv("QRT_COSET_OCC");
+        return (e && std::atoi(e) == 3) ? 3 : 2;
     }();
+    bool generic = false;
+    for (int i = 0; i < P.n_sets; ++i) generic = generic || P.sets[i].xbeg[31] < P.sets[i].g_count;
     static bool attr_done[64] = {};
     if (!attr_done[device]) {
-        QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
         QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
+        QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
+        QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
         attr_done[device] = true;
     }
     const std::size_t smem = (std::size_t{1} << kTileBits) * sizeof(double2) +
@@ -259,10 +256,12 @@ void launch_coset_pass(const CosetParams& P, const CosetDiagTerm* dterms, int pe
                              static_cast<std::size_t>(P.n_tab) * sizeof(double) +
                              (P.d_count > 0 ? (std::size_t{1} << kTileBits) * sizeof(double) : 0);
     dim3 grid(static_cast<unsigned>(P.tiles_per_pe), static_cast<unsigned>(pe_count));
-    if (gray)
+    if (generic)
         coset_pass_kernel<2, true><<<grid, kCosetThreads, smem, stream>>>(P, dterms, red);
-    else
+    else if (occ == 2)
         coset_pass_kernel<2, false><<<grid, kCosetThreads, smem, stream>>>(P, dterms, red);
+    else
+        coset_pass_kernel<3, false><<<grid, kCosetThreads, smem, stream>>>(P, dterms, red);
     QRT_CUDA(cudaGetLastError());
 }
 

@@ -27,7 +27,12 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <queue>
+#include <unordered_map>
+#include <unordered_set>
+#include <deque>
 #include <memory>
+#include <mutex>
 
 #include "qrt_coset.h"
 
@@ -467,7 +472,7 @@ bool coset_enabled() {
 void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B,
                       const std::vector<std::pair<std::uint64_t, std::vector<int>>>& flips, const std::vector<int>& gidx,
                       const std::vector<int>& diag, const std::uint64_t* y, const std::uint64_t* z,
-                      const std::uint64_t* gz, const double* coeffs) {
+                      const std::uint64_t* gz, const double* coeffs, const std::vector<std::uint64_t>* qsets) {
     int tile_pos[kTileBits], outer_pos[64], tb_of[64], ob_of[64];
     int ti = 0, no = 0;
     for (int p = 0; p < 64; ++p) tb_of[p] = ob_of[p] = -1;
@@ -520,10 +525,18 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
         return __builtin_popcount(static_cast<unsigned>(xt[static_cast<std::size_t>(a)])) >
                __builtin_popcount(static_cast<unsigned>(xt[static_cast<std::size_t>(b)]));
     });
+    std::size_t next_fixed = 0;
     while (!left.empty()) {
-        // ---- choose Q: 5 tile bits covering most remaining groups
+        // ---- choose Q: 5 tile bits covering most remaining groups (or the
+        // next set of the global cover, padded to 5 tile bits)
         int bestQ = 0, best = -1;
-        const std::size_t seeds = std::min<std::size_t>(12, left.size());
+        if (qsets && next_fixed < qsets->size()) {
+            bestQ = to_tile((*qsets)[next_fixed++]);
+            for (int b = kTileBits - 1; b >= 0 && __builtin_popcount(static_cast<unsigned>(bestQ)) < kCosetBits; --b)
+                bestQ |= 1 << b;
+            best = 0;
+        }
+        const std::size_t seeds = best >= 0 ? 0 : std::min<std::size_t>(12, left.size());
         for (std::size_t sd = 0; sd < seeds; ++sd) {
             const int x = xt[static_cast<std::size_t>(left[sd])];
             const int need = kCosetBits - __builtin_popcount(static_cast<unsigned>(x));
@@ -553,6 +566,7 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
         std::vector<int> in, keep;
         for (int g : left) ((xt[static_cast<std::size_t>(g)] & ~bestQ) == 0 ? in : keep).push_back(g);
         left.swap(keep);
+        if (in.empty()) continue;
         // ---- the set: register bits, thread bits (conflict-free lanes)
         CosetSet S{};
         int reg_of[kTileBits];
@@ -717,6 +731,59 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
 
 }  // namespace
 
+namespace {
+
+// Greedy cover of flip masks (weight <= 5) by sets of <= 5 positions, lazy
+// evaluation: a candidate's score is the number of still-uncovered masks
+// among its subsets.  Candidates: each mask united with an overlapping mask
+// (weight <= 5) or, for weight-4 masks, with one neighbouring position.
+// Returns the sets in pick order and, per set, the masks it took.
+std::vector<std::pair<std::uint64_t, std::vector<std::uint64_t>>> cover_masks(const std::vector<std::uint64_t>& masks) {
+    std::unordered_set<std::uint64_t> unc(masks.begin(), masks.end());
+    auto score = [&](std::uint64_t Q) {
+        int n = 0;
+        for (std::uint64_t sub = Q; sub; sub = (sub - 1) & Q) n += unc.count(sub) ? 1 : 0;
+        return n;
+    };
+    // neighbour positions of every mask: positions of overlapping masks
+    std::unordered_map<int, std::vector<std::uint64_t>> by_bit;
+    for (std::uint64_t m : masks)
+        for (std::uint64_t r = m; r; r &= r - 1) by_bit[__builtin_ctzll(r)].push_back(m);
+    std::unordered_set<std::uint64_t> cand;
+    for (std::uint64_t g : masks) {
+        cand.insert(g);
+        std::uint64_t nb = 0;
+        for (std::uint64_t r = g; r; r &= r - 1)
+            for (std::uint64_t h : by_bit[__builtin_ctzll(r)]) {
+                if (__builtin_popcountll(g | h) <= kCosetBits) cand.insert(g | h);
+                nb |= h;
+            }
+        if (__builtin_popcountll(g) == kCosetBits - 1)
+            for (std::uint64_t r = nb & ~g; r; r &= r - 1) cand.insert(g | (r & (~r + 1)));
+    }
+    std::priority_queue<std::pair<int, std::uint64_t>> heap;
+    for (std::uint64_t Q : cand) heap.emplace(score(Q), Q);
+    std::vector<std::pair<std::uint64_t, std::vector<std::uint64_t>>> out;
+    while (!unc.empty() && !heap.empty()) {
+        auto [sc, Q] = heap.top();
+        heap.pop();
+        const int now = score(Q);
+        if (now == 0) continue;
+        if (now < sc && !heap.empty() && now < heap.top().first) {
+            heap.emplace(now, Q);
+            continue;
+        }
+        std::vector<std::uint64_t> took;
+        for (std::uint64_t sub = Q; sub; sub = (sub - 1) & Q)
+            if (unc.erase(sub)) took.push_back(sub);
+        out.emplace_back(Q, std::move(took));
+    }
+    for (std::uint64_t m : unc) out.emplace_back(m, std::vector<std::uint64_t>{m});  // not reached in practice
+    return out;
+}
+
+}  // namespace
+
 // Host planning of one EVC tile: flip-mask groups, tile passes, coefficient
 // folding, and the wide (full-vector) groups.  No device access.
 PauliPlanHost build_pauli_plan(int nl, int pe_begin, int n_terms, const std::uint64_t* x, const std::uint64_t* y,
@@ -749,14 +816,85 @@ PauliPlanHost build_pauli_plan(int nl, int pe_begin, int n_terms, const std::uin
         std::uint64_t B;
         std::vector<int> groups;  // indices into flips
         bool has_diag;
+        std::vector<std::uint64_t> qsets;  // register sets of the global cover (coset passes)
     };
     std::vector<Pass> passes;
-    std::vector<int> left(flips.size());
-    for (std::size_t i = 0; i < flips.size(); ++i) left[i] = static_cast<int>(i);
+    bool global_cover = coset_enabled() && nl >= kTileBits && T == kTileBits && !flips.empty() && wide.empty();
+    {
+        const char* e = std::getenv("QRT_EVC_GLOBAL_COVER");
+        if (e && std::atoi(e) == 0) global_cover = false;
+    }
+    for (const auto& f : flips) global_cover = global_cover && popc(f.first) <= kCosetBits;
+    if (global_cover) {
+        // cover every flip mask by <= 5-position register sets, then pack the
+        // sets into tile passes (B holds the coalescing positions + 8 more)
+        std::vector<std::uint64_t> masks;
+        std::unordered_map<std::uint64_t, int> idx;
+        for (std::size_t i = 0; i < flips.size(); ++i) {
+            masks.push_back(flips[i].first);
+            idx[flips[i].first] = static_cast<int>(i);
+        }
+        auto sets = cover_masks(masks);
+        std::vector<std::size_t> rem(sets.size());
+        for (std::size_t i = 0; i < sets.size(); ++i) rem[i] = i;
+        const std::uint64_t coal_bits = (1ull << coal) - 1;
+        auto fill = [&](std::uint64_t b) {
+            for (int p = 0; p < nl && popc(b) < T; ++p) b |= 1ull << p;
+            return b;
+        };
+        bool first = true;
+        while (!rem.empty()) {
+            auto count = [&](std::uint64_t b) {
+                int n = 0;
+                for (std::size_t i : rem) n += (sets[i].first & ~b) == 0;
+                return n;
+            };
+            std::uint64_t B = 0;
+            int best = -1;
+            for (std::size_t sd = 0; sd < std::min<std::size_t>(16, rem.size()); ++sd) {
+                std::uint64_t b = coal_bits;
+                for (std::size_t q = 0; q < rem.size(); ++q) {
+                    const std::uint64_t m = sets[rem[(sd + q) % rem.size()]].first;
+                    if (popc(b | m) <= T) b |= m;
+                    if (popc(b) == T) break;
+                }
+                b = fill(b);
+                const int got = count(b);
+                if (got > best) {
+                    best = got;
+                    B = b;
+                }
+            }
+            for (int w = coal; w + (T - coal) <= nl; ++w) {
+                const std::uint64_t b = coal_bits | (((1ull << (T - coal)) - 1) << w);
+                const int got = count(b);
+                if (got > best) {
+                    best = got;
+                    B = b;
+                }
+            }
+            Pass ps{B, {}, first && !diag.empty(), {}};
+            first = false;
+            std::vector<std::size_t> keep;
+            for (std::size_t i : rem) {
+                if (sets[i].first & ~B) {
+                    keep.push_back(i);
+                    continue;
+                }
+                ps.qsets.push_back(sets[i].first);
+                for (std::uint64_t m : sets[i].second) ps.groups.push_back(idx[m]);
+            }
+            if (ps.qsets.empty()) fail(QRT_ERR_INVALID, "EVC set packing made no progress");
+            passes.push_back(std::move(ps));
+            rem.swap(keep);
+        }
+    }
+    std::vector<int> left(global_cover ? 0 : flips.size());
+    for (std::size_t i = 0; i < left.size(); ++i) left[i] = static_cast<int>(i);
     std::stable_sort(left.begin(), left.end(), [&](int a, int b) {
         return popc(flips[static_cast<std::size_t>(a)].first) > popc(flips[static_cast<std::size_t>(b)].first);
     });
-    bool diag_done = diag.empty();
+    bool diag_done = diag.empty() || global_cover;
     while (!left.empty() || !diag_done) {
         std::uint64_t B = (1ull << coal) - 1;
         if (T == nl) {
@@ -818,7 +956,7 @@ PauliPlanHost build_pauli_plan(int nl, int pe_begin, int n_terms, const std::uin
             if (popc(flips[static_cast<std::size_t>(gi)].first) > kCosetBits) coset = false;
         if (coset) {
             build_coset_pass(plan, nl, pe_begin, ps.B, flips, ps.groups, ps.has_diag ? diag : std::vector<int>{}, y, z,
-                             gz, coeffs);
+                             gz, coeffs, ps.qsets.empty() ? nullptr : &ps.qsets);
             continue;
         }
         PPass h{};
@@ -939,7 +1077,31 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
     for (int i = 0; i < 2 * st->p; ++i) partial[i] = 0.0;
     if (n_terms == 0) return;
 
-    PauliPlanHost plan = build_pauli_plan(nl, st->pe_begin, n_terms, x, y, z, gz, coeffs);
+    // A VQE loop evaluates the same Hamiltonian under the same layout every
+    // iteration: plans are cached by their exact inputs.
+    static std::mutex cache_mu;
+    static std::deque<std::pair<std::vector<std::uint64_t>, std::shared_ptr<PauliPlanHost>>> cache;
+    std::vector<std::uint64_t> key;
+    key.reserve(3 + 6 * static_cast<std::size_t>(n_terms));
+    key.push_back(static_cast<std::uint64_t>(nl));
+    key.push_back(static_cast<std::uint64_t>(st->pe_begin));
+    key.push_back(static_cast<std::uint64_t>(n_terms));
+    for (int t = 0; t < n_terms; ++t) {
+        std::uint64_t cr, ci;
+        std::memcpy(&cr, coeffs + 2 * t, 8);
+        std::memcpy(&ci, coeffs + 2 * t + 1, 8);
+        key.insert(key.end(), {x[t], y[t], z[t], gz[t], cr, ci});
+    }
+    std::lock_guard<std::mutex> lock(cache_mu);
+    std::shared_ptr<PauliPlanHost> plan_ptr;
+    for (auto& e : cache)
+        if (e.first == key) plan_ptr = e.second;
+    if (!plan_ptr) {
+        plan_ptr = std::make_shared<PauliPlanHost>(build_pauli_plan(nl, st->pe_begin, n_terms, x, y, z, gz, coeffs));
+        cache.emplace_back(std::move(key), plan_ptr);
+        if (cache.size() > 8) cache.pop_front();
+    }
+    PauliPlanHost& plan = *plan_ptr;
     const int T = plan.T;
     auto& dgroups = plan.dgroups;
     auto& dterms = plan.dterms;

@@ -1032,6 +1032,18 @@ GatePlan plan_gates(int nl, int n_gates, const int* arity, const int* pos, const
                 }
             }
             if (env_on("QRT_MERGE_SIGNS", true)) n_ops = merge_sign_ops(L->ops, S.op_begin, n_ops);
+            for (int o = S.op_begin; o < n_ops; ++o) {
+                LightOp& lo = L->ops[o];
+                int code = kCodeDiag;
+                if (lo.kind == kL1) code = lo.q0;
+                else if (lo.kind == kL2) {
+                    static const int pair_code[4][4] = {{-1, 4, 5, 6}, {-1, -1, 7, 8}, {-1, -1, -1, 9}, {-1, -1, -1, -1}};
+                    code = pair_code[lo.q0][lo.q1];
+                } else if (lo.kind == kLSignU) code = kCodeSignU;
+                else if (lo.kind == kLSignS) code = kCodeSignS;
+                else if (lo.kind == kLSignG) code = kCodeSignG;
+                lo.code = static_cast<std::int8_t>(code | (lo.flush ? kCodeFlush : 0));
+            }
             S.op_count = static_cast<std::int16_t>(n_ops - S.op_begin);
         }
         if (n_ops > kLightMaxOps || n_mats > kLightMaxMats) fail(QRT_ERR_INVALID, "light pass over budget");

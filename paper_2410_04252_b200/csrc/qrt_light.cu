@@ -65,17 +65,6 @@ __device__ __forceinline__ void dense2(double2 (&a)[16], const double2* __restri
     }
 }
 
-__device__ __forceinline__ void apply_dense2(double2 (&a)[16], const double2* m, int q0, int q1) {
-    switch (q0 * 4 + q1) {
-        case 1: dense2<0, 1>(a, m); break;
-        case 2: dense2<0, 2>(a, m); break;
-        case 3: dense2<0, 3>(a, m); break;
-        case 6: dense2<1, 2>(a, m); break;
-        case 7: dense2<1, 3>(a, m); break;
-        default: dense2<2, 3>(a, m); break;
-    }
-}
-
 // Pending +-1 signs: bit r set = register slot r still owes a negation.
 // Applied by XOR on the sign bits (integer pipe), not as fp64 negations.
 __device__ __forceinline__ void apply_signs(double2 (&a)[16], unsigned& pend) {
@@ -216,45 +205,46 @@ __global__ void __launch_bounds__(kLightThreads, 2) light_pass_kernel(const __gr
         const int o_end = S.op_begin + S.op_count;
         for (int o = S.op_begin; o < o_end; ++o) {
             const LightOp& op = P.ops[o];
-            const int kind = op.kind;
-            if (kind == kLSignU) {
-                g ^= static_cast<unsigned>(op.tab >> fixed_value(op, W)) & 1u;
-                continue;
-            }
-            if (kind == kLSignS) {
-                pend ^= static_cast<unsigned>(op.tab >> (16 * fixed_value(op, W))) & 0xffffu;
-                continue;
-            }
-            if (op.flush) apply_signs(a, pend);
-            if (kind == kL1) {
-                const double2* m = P.mats + op.mat;
-                switch (op.q0) {
-                    case 0: dense1<0>(a, m); break;
-                    case 1: dense1<1>(a, m); break;
-                    case 2: dense1<2>(a, m); break;
-                    default: dense1<3>(a, m); break;
+            // one host-computed case code per op (jump table), flush bit on top
+            const int code = op.code;
+            if (code & kCodeFlush) apply_signs(a, pend);
+            switch (code & ~kCodeFlush) {
+                case 0: dense1<0>(a, P.mats + op.mat); break;
+                case 1: dense1<1>(a, P.mats + op.mat); break;
+                case 2: dense1<2>(a, P.mats + op.mat); break;
+                case 3: dense1<3>(a, P.mats + op.mat); break;
+                case 4: dense2<0, 1>(a, P.mats + op.mat); break;
+                case 5: dense2<0, 2>(a, P.mats + op.mat); break;
+                case 6: dense2<0, 3>(a, P.mats + op.mat); break;
+                case 7: dense2<1, 2>(a, P.mats + op.mat); break;
+                case 8: dense2<1, 3>(a, P.mats + op.mat); break;
+                case 9: dense2<2, 3>(a, P.mats + op.mat); break;
+                case kCodeSignU: g ^= static_cast<unsigned>(op.tab >> fixed_value(op, W)) & 1u; break;
+                case kCodeSignS: pend ^= static_cast<unsigned>(op.tab >> (16 * fixed_value(op, W))) & 0xffffu; break;
+                case kCodeSignG: {
+                    const int f = fixed_value(op, W);
+                    unsigned mask = 0;
+#pragma unroll
+                    for (int r = 0; r < 16; ++r)
+                        mask |= static_cast<unsigned>((op.tab >> diag_index(op, f, r)) & 1ull) << r;
+                    pend ^= mask;
+                    break;
                 }
-            } else if (kind == kL2) {
-                apply_dense2(a, P.mats + op.mat, op.q0, op.q1);
-            } else if (kind == kLSignG) {
-                const int f = fixed_value(op, W);
-                unsigned mask = 0;
-#pragma unroll
-                for (int r = 0; r < 16; ++r) mask |= static_cast<unsigned>((op.tab >> diag_index(op, f, r)) & 1ull) << r;
-                pend ^= mask;
-            } else {
-                // phase diagonal (k <= 2): two entries live at a time
-                const int f = fixed_value(op, W);
-                const double2* d = P.mats + op.mat;
-                const int halves = op.k > 1 ? 2 : 1;
+                default: {
+                    // phase diagonal (k <= 2): two entries live at a time
+                    const int f = fixed_value(op, W);
+                    const double2* d = P.mats + op.mat;
+                    const int halves = op.k > 1 ? 2 : 1;
 #pragma unroll 1
-                for (int hb = 0; hb < halves; ++hb) {
-                    const double2 d0 = d[2 * hb], d1 = d[2 * hb + 1];
+                    for (int hb = 0; hb < halves; ++hb) {
+                        const double2 d0 = d[2 * hb], d1 = d[2 * hb + 1];
 #pragma unroll
-                    for (int r = 0; r < 16; ++r) {
-                        const int m = diag_index(op, f, r);
-                        if ((m >> 1) == hb) a[r] = cmul((m & 1) ? d1 : d0, a[r]);
+                        for (int r = 0; r < 16; ++r) {
+                            const int m = diag_index(op, f, r);
+                            if ((m >> 1) == hb) a[r] = cmul((m & 1) ? d1 : d0, a[r]);
+                        }
                     }
+                    break;
                 }
             }
         }

@@ -42,6 +42,11 @@ inline constexpr int kLightMaxDiagK = 6;
 // kLSignG:   any other +-1 diagonal (k <= 6): slot mask evaluated per slot.
 enum LightKind : std::int8_t { kL1 = 0, kL2 = 1, kLDiag = 2, kLSignU = 3, kLSignS = 4, kLSignG = 5 };
 
+// LightOp::code: 0-3 dense 1-qubit on register bit q; 4-9 dense 2-qubit on
+// register-bit pair (0,1) (0,2) (0,3) (1,2) (1,3) (2,3); then the diagonal
+// kinds; kCodeFlush set = apply pending slot signs first.
+inline constexpr int kCodeSignU = 10, kCodeSignS = 11, kCodeSignG = 12, kCodeDiag = 13, kCodeFlush = 64;
+
 struct LightOp {
     std::uint64_t tab;  // kLSignU: bit f = sign of fixed-bit value f; kLSignS: 16-bit slot masks per f;
                         // kLSignG: the -1 entries of the diagonal
@@ -49,6 +54,7 @@ struct LightOp {
     std::int8_t kind, k;
     std::int8_t q0, q1;  // dense: register bits of matrix bits 0 / 1 (q0 < q1 for kL2)
     std::int8_t flush;   // apply pending slot signs before this op
+    std::int8_t code;    // dispatch case (see kCode*), computed on the host
     std::int8_t nsrc;    // fixed (non-register) targets
     std::int8_t src[kLightMaxDiagK];  // bit of the thread word W holding fixed target i
     std::int8_t rq[kLightMaxDiagK];   // kLDiag/kLSignG: register bit of target j, 4 if fixed

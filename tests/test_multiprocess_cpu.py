@@ -1,4 +1,4 @@
-"""N>1 host logic on CPU: two gloo ranks (one per "GPU") emulate the
+"""N>1 host logic on CPU: 2, 4 or 8 gloo ranks (one per "GPU") emulate the
 distributed QR exactly as libqrt performs it — PE ownership (rank r owns PEs
 [r*p/w, (r+1)*p/w)), the physical placement chosen by physical_reorder_plan,
 and the kernel's own destination mapping replayed by qrt_reorder_plan — and
@@ -101,17 +101,19 @@ def _worker(rank, world, port, n, p, seed, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,p,seed", [(8, 2, 1), (10, 4, 2), (11, 8, 3)])
-def test_two_rank_reorder_matches_oracle(n, p, seed):
+@pytest.mark.parametrize("world,n,p,seed", [(2, 8, 2, 1), (2, 10, 4, 2), (2, 11, 8, 3), (4, 10, 4, 4), (8, 12, 8, 5)])
+def test_multi_rank_reorder_matches_oracle(world, n, p, seed):
+    """world = 8, p = 8 is the one-PE-per-GPU layout of an 8xB200 box (every
+    lazy QR there swaps all three global bits: an 8-way all-to-all)."""
     import multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, p, seed, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, p, seed, q)) for r in range(world)]
     for pr in procs:
         pr.start()
-    results = dict(q.get(timeout=240) for _ in procs)
+    results = dict(q.get(timeout=300) for _ in procs)
     for pr in procs:
         pr.join(timeout=60)
-    assert results == {0: True, 1: True}
+    assert results == {r: True for r in range(world)}

@@ -18,10 +18,14 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <array>
 #include <iterator>
+#include <deque>
 #include <memory>
+#include <mutex>
 
 #include "qrt_light.h"
 
@@ -533,6 +537,43 @@ struct LightStagePlan {
     std::vector<int> ops;
 };
 
+// DMMA B-fragment layout of M^T for a dense k-qubit gate, M = the 2D x 2D
+// real form of U ([[Re, -Im], [Im, Re]] blocks): for fragment slot
+// ((nb * KB + kb) * 32 + lane), the interleaved payload index and the sign.
+// PTX m8n8k4.f64 B fragment: row k = lane & 3, column n = lane >> 2.
+std::vector<std::pair<int, double>> frag_map(int k) {
+    const int D = 1 << k, R = 2 * D, NB = R / 8, KB = R / 4;
+    std::vector<std::pair<int, double>> m;
+    for (int nb = 0; nb < NB; ++nb)
+        for (int kb = 0; kb < KB; ++kb)
+            for (int lane = 0; lane < 32; ++lane) {
+                const int kk = 4 * kb + (lane & 3), nn = 8 * nb + (lane >> 2);
+                const int r = nn >> 1, i = nn & 1, c = kk >> 1, j = kk & 1;
+                const int at = 2 * (r * D + c);
+                if (i == j)
+                    m.emplace_back(at, 1.0);  // Re
+                else
+                    m.emplace_back(at + 1, i == 0 ? -1.0 : 1.0);  // -Im / +Im
+            }
+    return m;
+}
+
+// Per-thread storage recycled between calls for the DMMA fragment pool.
+std::vector<double>& frag_storage() {
+    static thread_local std::vector<double> v;
+    return v;
+}
+
+// One HBM pass of a gate plan (structure only; payloads are packed later).
+struct GatePass {
+    bool wide = false;
+    bool light = false;
+    int T = 0, c = 0;
+    std::vector<int> tile_pos;
+    std::vector<int> ops;
+    std::vector<LightStagePlan> stages;
+};
+
 int plan_light_stages(const std::vector<HostOp>& opsv, const std::vector<int>& taken, std::uint64_t B, int m_max,
                       std::vector<LightStagePlan>* out, std::vector<int>* leftover) {
     std::vector<int> rem = taken, keep;
@@ -614,6 +655,13 @@ struct GatePlan {
 
 GatePlan plan_gates(int nl, int n_gates, const int* arity, const int* pos, const double* mats, const unsigned* flags) {
     GatePlan plan;
+    auto T0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!std::getenv("QRT_DEBUG_PLAN")) return;
+        auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "  %s %.3f ms\n", what, std::chrono::duration<double, std::milli>(t - T0).count());
+        T0 = t;
+    };
     const double amps_all = 1.0;  // flops are accumulated per amplitude
     // ---- decode and validate -------------------------------------------------
     std::vector<HostOp> opsv(static_cast<std::size_t>(n_gates));
@@ -711,16 +759,40 @@ GatePlan plan_gates(int nl, int n_gates, const int* arity, const int* pos, const
         }
     }
 
+    lap("decode+fuse");
     // ---- plan passes -----------------------------------------------------------
-    struct Pass {
-        bool wide = false;
-        bool light = false;
-        int T = 0, c = 0;
-        std::vector<int> tile_pos;
-        std::vector<int> ops;
-        std::vector<LightStagePlan> stages;
-    };
+    // The decomposition depends only on the gate structure (arity, positions,
+    // kinds after fusion, sign classification), not on payload values: a VQE
+    // loop re-applies the same circuit with new angles every iteration, so it
+    // is cached by that structure and only the payloads are re-packed below.
+    using Pass = GatePass;
+    std::vector<std::uint64_t> skey;
+    skey.reserve(4 + 4 * static_cast<std::size_t>(n_gates));
+    skey.push_back(static_cast<std::uint64_t>(nl));
+    skey.push_back(static_cast<std::uint64_t>(n_gates));
+    skey.push_back((nl >= kTileBits && env_on("QRT_LIGHT", true) ? 1u : 0u) | (static_cast<unsigned>(light_max_stages()) << 1));
+    for (int i = 0; i < n_gates; ++i) {
+        const HostOp& h = opsv[static_cast<std::size_t>(i)];
+        std::uint64_t w = static_cast<std::uint64_t>(h.k) | (static_cast<std::uint64_t>(h.kind) << 8) |
+                          (static_cast<std::uint64_t>(dead[static_cast<std::size_t>(i)]) << 9) |
+                          (static_cast<std::uint64_t>(h.sign) << 10) | (static_cast<std::uint64_t>(h.mat_len) << 16);
+        skey.push_back(w);
+        skey.push_back(h.mask);
+        skey.push_back(h.sign ? h.neg : 0);
+        std::uint64_t order = 0;
+        for (int j = 0; j < h.k && j < 10; ++j) order |= static_cast<std::uint64_t>(h.pos[j]) << (6 * j);
+        skey.push_back(order);
+    }
+    static std::mutex plan_mu;
+    static std::deque<std::pair<std::vector<std::uint64_t>, std::shared_ptr<const std::vector<GatePass>>>> plan_cache;
+    std::shared_ptr<const std::vector<GatePass>> cached;
+    if (env_on("QRT_PLAN_CACHE", true)) {
+        std::lock_guard<std::mutex> lock(plan_mu);
+        for (auto& e : plan_cache)
+            if (e.first == skey) cached = e.second;
+    }
     std::vector<Pass> passes;
+    if (cached) passes = *cached;
     std::vector<int> remaining;
     remaining.reserve(static_cast<std::size_t>(n_gates));
     for (int i = 0; i < n_gates; ++i)
@@ -845,6 +917,7 @@ GatePlan plan_gates(int nl, int n_gates, const int* arity, const int* pos, const
         for (int p = 0; p < nl && __builtin_popcountll(B) < kTileBits; ++p) B |= 1ull << p;
         return B;
     };
+    if (cached) remaining.clear();
     while (!remaining.empty()) {
         std::uint64_t B = 0;
         if (whole) {
@@ -876,7 +949,13 @@ GatePlan plan_gates(int nl, int n_gates, const int* arity, const int* pos, const
         passes.push_back(std::move(ps));
         remaining.swap(keep);
     }
+    if (!cached && env_on("QRT_PLAN_CACHE", true)) {
+        std::lock_guard<std::mutex> lock(plan_mu);
+        plan_cache.emplace_back(std::move(skey), std::make_shared<const std::vector<GatePass>>(passes));
+        if (plan_cache.size() > 16) plan_cache.pop_front();
+    }
 
+    lap("plan");
     // ---- pack descriptors + matrices into one upload ------------------------------
     std::vector<GateOp>& dev_ops = plan.dev_ops;
     std::vector<PassHdr>& hdrs = plan.hdrs;
@@ -884,6 +963,20 @@ GatePlan plan_gates(int nl, int n_gates, const int* arity, const int* pos, const
     std::vector<std::vector<double2>>& pmats = plan.pmats;
     pmats.resize(passes.size());
     std::vector<double>& frags = plan.frags;
+    {
+        // reuse the previous call's storage (no page faults on ~14 MB of
+        // fragments per call) and size it exactly
+        frags.swap(frag_storage());
+        frags.clear();
+        std::size_t need = 0;
+        for (const auto& ps : passes)
+            if (!ps.light && !ps.wide)
+                for (int id : ps.ops) {
+                    const HostOp& o = opsv[static_cast<std::size_t>(id)];
+                    if (o.kind == kDense && (o.k == 3 || o.k == 4) && ps.T >= o.k + 3) need += 4u * o.mat_len;
+                }
+        frags.reserve(need);
+    }
     std::vector<int>& wide_pos = plan.wide_pos;  // for wide passes: positions (kBigK per pass)
     std::vector<std::unique_ptr<LightParams>>& light = plan.light;
     auto build_light = [&](const std::vector<int>& tile_pos, int c, const std::vector<LightStagePlan>& stages) {
@@ -1120,17 +1213,15 @@ GatePlan plan_gates(int nl, int n_gates, const int* arity, const int* pos, const
                 staged += o.mat_len;
             } else if ((o.k == 3 || o.k == 4) && ps.T >= o.k + 3) {
                 // DMMA B fragments of M^T, M = real form of U (see dense_dmma)
-                const int D = 1 << o.k, R = 2 * D, NB = R / 8, KB = R / 4;
+                const int D = 1 << o.k, R = 2 * D;
                 g.bfrag = static_cast<int>(frags.size()) - h.frag_begin;
-                for (int nb = 0; nb < NB; ++nb)
-                    for (int kb = 0; kb < KB; ++kb)
-                        for (int lane = 0; lane < 32; ++lane) {
-                            const int kk = 4 * kb + (lane & 3), nn = 8 * nb + (lane >> 2);
-                            const int r = nn >> 1, i = nn & 1, c = kk >> 1, j = kk & 1;
-                            const std::size_t at = 2 * (static_cast<std::size_t>(r) * D + c);
-                            const double re = o.m[at], im = o.m[at + 1];
-                            frags.push_back(i == j ? re : (i == 0 ? -im : im));
-                        }
+                // fragment slot -> (interleaved source index, sign), built once per k
+                static const std::vector<std::pair<int, double>> map3 = frag_map(3), map4 = frag_map(4);
+                const auto& fm = o.k == 3 ? map3 : map4;
+                const std::size_t at = frags.size();
+                frags.resize(at + static_cast<std::size_t>(R) * R);
+                double* dst = frags.data() + at;
+                for (std::size_t e = 0; e < fm.size(); ++e) dst[e] = fm[e].second * o.m[fm[e].first];
             } else if (o.k <= 4) {
                 g.pmat = static_cast<int>(pmats[pidx].size());
                 put(pmats[pidx], o);
@@ -1147,6 +1238,7 @@ GatePlan plan_gates(int nl, int n_gates, const int* arity, const int* pos, const
         }
         hdrs.push_back(h);
     }
+    lap("pack");
     return plan;
 }
 
@@ -1164,6 +1256,10 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
     const auto& frags = plan.frags;
     const auto& wide_pos = plan.wide_pos;
     auto& light = plan.light;
+    struct GiveBack {
+        std::vector<double>& f;
+        ~GiveBack() { frag_storage().swap(f); }
+    } give_back{plan.frags};
     const std::size_t ops_bytes = dev_ops.size() * sizeof(GateOp);
     const std::size_t pool_off = (ops_bytes + 255) & ~std::size_t{255};
     const std::size_t pool_bytes = pool.size() * sizeof(double2);

@@ -182,3 +182,27 @@ def test_light_sign_merging(qb, device, merge, monkeypatch):
     for op in ops:
         cpu.apply_gate(sub, list(op.targets), op.payload)
     assert float(np.max(np.abs(_sub(st) - sub))) <= AMP_TOL
+
+
+def test_plan_cache_repacks_new_angles(qb, device):
+    """A VQE loop: same circuit structure, new angles every iteration.  The
+    cached pass decomposition must be re-packed with the new payloads."""
+    n = 16
+    for seed in (3, 4, 3, 5):
+        c = qb.gen_hea(n, 6, seed, True)
+        st = qb.init_state(n, qb.ClusterShape.flat(1))
+        qb.apply_gates_narrow(st, c, list(range(c.size())))
+        sub = np.zeros((1, 1 << n), dtype=complex)
+        sub[0, 0] = 1
+        for op in c.operators:
+            cpu.apply_gate(sub, list(op.targets), op.payload)
+        assert float(np.max(np.abs(_sub(st) - sub))) <= AMP_TOL, seed
+    for seed in (7, 8):  # GateFabric (DMMA fragments re-packed)
+        c = qb.gen_gatefabric(14, 8, seed, True)
+        st = qb.init_state(14, qb.ClusterShape.flat(1))
+        qb.apply_gates_narrow(st, c, list(range(c.size())))
+        sub = np.zeros((1, 1 << 14), dtype=complex)
+        sub[0, 0] = 1
+        for op in c.operators:
+            cpu.apply_gate(sub, list(op.targets), op.payload)
+        assert float(np.max(np.abs(_sub(st) - sub))) <= AMP_TOL, seed

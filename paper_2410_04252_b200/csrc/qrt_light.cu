@@ -40,6 +40,22 @@ __device__ __forceinline__ void dense1(double2 (&a)[16], const double2* __restri
     }
 }
 
+// Dense 1-qubit gate whose first column is real (m00, m10 real): 6 fp64
+// operations per amplitude instead of 8.
+template <int Q>
+__device__ __forceinline__ void dense1r(double2 (&a)[16], const double2* __restrict__ m) {
+    const double m00 = m[0].x, m10 = m[2].x;
+    const double2 m01 = m[1], m11 = m[3];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        if ((r >> Q) & 1) continue;
+        const int s = r | (1 << Q);
+        const double2 x = a[r], y = a[s];
+        a[r] = make_double2(fma(m00, x.x, fma(m01.x, y.x, -m01.y * y.y)), fma(m00, x.y, fma(m01.x, y.y, m01.y * y.x)));
+        a[s] = make_double2(fma(m10, x.x, fma(m11.x, y.x, -m11.y * y.y)), fma(m10, x.y, fma(m11.x, y.y, m11.y * y.x)));
+    }
+}
+
 // Matrix bit 0 <-> register bit Q0, matrix bit 1 <-> register bit Q1 (Q0 < Q1).
 template <int Q0, int Q1>
 __device__ __forceinline__ void dense2(double2 (&a)[16], const double2* __restrict__ m) {
@@ -219,6 +235,10 @@ __global__ void __launch_bounds__(kLightThreads, 2) light_pass_kernel(const __gr
                 case 7: dense2<1, 2>(a, P.mats + op.mat); break;
                 case 8: dense2<1, 3>(a, P.mats + op.mat); break;
                 case 9: dense2<2, 3>(a, P.mats + op.mat); break;
+                case kCodeReal1 + 0: dense1r<0>(a, P.mats + op.mat); break;
+                case kCodeReal1 + 1: dense1r<1>(a, P.mats + op.mat); break;
+                case kCodeReal1 + 2: dense1r<2>(a, P.mats + op.mat); break;
+                case kCodeReal1 + 3: dense1r<3>(a, P.mats + op.mat); break;
                 case kCodeSignU: g ^= static_cast<unsigned>(op.tab >> fixed_value(op, W)) & 1u; break;
                 case kCodeSignS: pend ^= static_cast<unsigned>(op.tab >> (16 * fixed_value(op, W))) & 0xffffu; break;
                 case kCodeSignG: {

@@ -44,8 +44,10 @@ enum LightKind : std::int8_t { kL1 = 0, kL2 = 1, kLDiag = 2, kLSignU = 3, kLSign
 
 // LightOp::code: 0-3 dense 1-qubit on register bit q; 4-9 dense 2-qubit on
 // register-bit pair (0,1) (0,2) (0,3) (1,2) (1,3) (2,3); then the diagonal
-// kinds; kCodeFlush set = apply pending slot signs first.
-inline constexpr int kCodeSignU = 10, kCodeSignS = 11, kCodeSignG = 12, kCodeDiag = 13, kCodeFlush = 64;
+// kinds; 14-17 dense 1-qubit with a real first column (phase-folded) on
+// register bit q; kCodeFlush set = apply pending slot signs first.
+inline constexpr int kCodeSignU = 10, kCodeSignS = 11, kCodeSignG = 12, kCodeDiag = 13, kCodeReal1 = 14,
+                     kCodeFlush = 64;
 
 struct LightOp {
     std::uint64_t tab;  // kLSignU: bit f = sign of fixed-bit value f; kLSignS: 16-bit slot masks per f;
@@ -55,6 +57,7 @@ struct LightOp {
     std::int8_t q0, q1;  // dense: register bits of matrix bits 0 / 1 (q0 < q1 for kL2)
     std::int8_t flush;   // apply pending slot signs before this op
     std::int8_t code;    // dispatch case (see kCode*), computed on the host
+    std::int8_t realcol; // kL1: first column real
     std::int8_t nsrc;    // fixed (non-register) targets
     std::int8_t src[kLightMaxDiagK];  // bit of the thread word W holding fixed target i
     std::int8_t rq[kLightMaxDiagK];   // kLDiag/kLSignG: register bit of target j, 4 if fixed

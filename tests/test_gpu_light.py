@@ -76,8 +76,8 @@ def test_light_random_runs_vs_oracle(qb, device, n, p, count, seed):
 @pytest.mark.parametrize("stages", ["1", "2", "8"])
 @pytest.mark.parametrize("fuse", ["0", "1"])
 def test_light_stage_and_fusion_knobs(qb, device, stages, fuse, monkeypatch):
-    """QRT_FUSE_1Q is read per call; QRT_LIGHT_STAGES once per process, so the
-    stage counts here run in a subprocess."""
+    """QRT_FUSE_1Q / QRT_PHASE_FOLD are read per call; QRT_LIGHT_STAGES once per
+    process, so the stage counts here run in a subprocess."""
     if stages != "1":
         import subprocess
         import sys
@@ -103,6 +103,7 @@ def test_light_stage_and_fusion_knobs(qb, device, stages, fuse, monkeypatch):
         assert res.returncode == 0, res.stdout + res.stderr
         return
     monkeypatch.setenv("QRT_FUSE_1Q", fuse)
+    monkeypatch.setenv("QRT_PHASE_FOLD", fuse)  # row-phase folding on/off with fusion
     n = 15
     c = qb.gen_hea(n, 5, 11, True)
     st = qb.init_state(n, qb.ClusterShape.flat(1))

@@ -82,3 +82,39 @@ def test_coset_deterministic(qb, device):
     plan = qb.plan_evc(terms, n, shape, True)
     e = [qb.expectation(qb.init_state_from(psi, shape), plan, terms) for _ in range(3)]
     assert e[0] == e[1] == e[2]
+
+
+@pytest.mark.parametrize("env", [{"QRT_EVC_GLOBAL_COVER": "0"}, {"QRT_COSET_OCC": "3"}, {"QRT_GATE_THREADS": "256"},
+                                 {"QRT_PLAN_CACHE": "0"}])
+def test_knobs_in_subprocess(env):
+    """Knobs read once per process: a fresh process per setting, checked
+    against the oracle (GateFabric QSU + JW EVC at 16 qubits, 2 PEs)."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, sys\n"
+        "sys.path.insert(0, '.'); sys.path.insert(0, 'tests')\n"
+        "import paper_2410_04252_b200 as qb\n"
+        "from oracle import cpu\n"
+        "from test_gpu_parity import oracle_expectation\n"
+        "qb.init_device(0, 1, 0)\n"
+        "n, p = 16, 2\n"
+        "c = qb.gen_gatefabric(n, 8, 2, True)\n"
+        "shape = qb.ClusterShape.flat(p)\n"
+        "s = qb.flat_tiling(c, qb.build_dependency_graph(c), shape)\n"
+        "st = qb.init_state(n, shape); qb.run_qsu(st, c, s)\n"
+        "sub, lay, _ = cpu.run_qsu(n, p, c, s)\n"
+        "psi = cpu.flatten(sub, lay.qubit_at)\n"
+        "assert float(np.max(np.abs(qb.flatten(st) - psi))) <= 1e-12\n"
+        "terms = qb.gen_synthetic_jw(n, 3, 10)\n"
+        "plan = qb.plan_evc(terms, n, shape, True)\n"
+        "e = qb.expectation(qb.init_state_from(psi, shape), plan, terms)\n"
+        "w = oracle_expectation(qb, psi, n, p, terms, plan)\n"
+        "assert abs(e - w) <= 1e-10 * (1 + abs(w)), (e, w)\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), cwd=root, capture_output=True,
+                         text=True, timeout=300)
+    assert res.returncode == 0, res.stdout + res.stderr

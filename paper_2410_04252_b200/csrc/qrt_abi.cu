@@ -406,6 +406,7 @@ qrt_status qrt_state_destroy(qrt_state* st) {
     TraceScope trace_("qrt_state_destroy");
     return guarded([&] {
         if (!st) return;
+        st->qr_pending = false;
         {
             DeviceGuard g(st->device);
             QRT_CUDA(cudaStreamSynchronize(st->stream));
@@ -440,6 +441,7 @@ qrt_status qrt_state_set_zero(qrt_state* st) {
     return guarded([&] {
         require(st != nullptr, QRT_ERR_INVALID, "null state");
         DeviceGuard g(st->device);
+        st->qr_pending = false;  // |0...0> is the same in every layout
         for (int i = 0; i < st->pe_count; ++i)
             zero_state_kernel<<<grid_for(st->amps, 256), 256, 0, st->stream>>>(st->live(i), st->amps,
                                                                                st->pe_begin + i == 0);
@@ -455,6 +457,7 @@ qrt_status qrt_state_upload(qrt_state* st, int pe, const double* amps) {
         require(st && amps, QRT_ERR_INVALID, "null argument");
         require(pe >= st->pe_begin && pe < st->pe_begin + st->pe_count, QRT_ERR_INVALID, "PE not owned by this process");
         DeviceGuard g(st->device);
+        flush_reorder(st);
         QRT_CUDA(cudaMemcpyAsync(st->live(pe - st->pe_begin), amps, st->amps * sizeof(amp_t), cudaMemcpyHostToDevice,
                                  st->stream));
         QRT_CUDA(cudaStreamSynchronize(st->stream));
@@ -467,6 +470,7 @@ qrt_status qrt_state_download(const qrt_state* st, int pe, double* amps) {
         require(st && amps, QRT_ERR_INVALID, "null argument");
         require(pe >= st->pe_begin && pe < st->pe_begin + st->pe_count, QRT_ERR_INVALID, "PE not owned by this process");
         DeviceGuard g(st->device);
+        flush_reorder(const_cast<qrt_state*>(st));
         QRT_CUDA(cudaMemcpyAsync(amps, st->live(pe - st->pe_begin), st->amps * sizeof(amp_t), cudaMemcpyDeviceToHost,
                                  st->stream));
         QRT_CUDA(cudaStreamSynchronize(st->stream));
@@ -517,6 +521,7 @@ qrt_status qrt_pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t
         require(n_terms == 0 || (x && y && z && gz && coeffs), QRT_ERR_INVALID, "null term arrays");
         DeviceGuard g(st->device);
         st->stats[QRT_K_PAULI].calls++;
+        flush_reorder(st);
         pauli_expectation(st, n_terms, x, y, z, gz, coeffs, partial);
     });
 }
@@ -544,6 +549,7 @@ qrt_status qrt_norm(qrt_state* st, double* out) {
     return guarded([&] {
         require(st && out, QRT_ERR_INVALID, "null argument");
         DeviceGuard g(st->device);
+        flush_reorder(st);
         *out = norm(st);
     });
 }

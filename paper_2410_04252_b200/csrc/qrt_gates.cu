@@ -28,6 +28,7 @@
 #include <memory>
 #include <mutex>
 
+#include "qrt_fused.h"
 #include "qrt_light.h"
 
 namespace qrt {
@@ -323,7 +324,7 @@ __device__ __forceinline__ void diagonal(double2* __restrict__ tile, const doubl
 // through L1 (they are shared by every CTA of the pass).
 __global__ void __launch_bounds__(256, 2)
     gate_pass_kernel(const __grid_constant__ PassParams P, const double2* __restrict__ pool,
-                     const double* __restrict__ frags, int tiles_per_pe) {
+                     const double* __restrict__ frags, int tiles_per_pe, const FusedSource* __restrict__ fs) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const PassHdr& hdr = P.hdr;
     const int T = hdr.T, E = 1 << T, c = hdr.c;
@@ -347,7 +348,14 @@ __global__ void __launch_bounds__(256, 2)
 
     amp_t* __restrict__ v = P.ptrs.p[t / tiles_per_pe];
     const int cmask = (1 << c) - 1;
-    for (int e = threadIdx.x; e < E; e += blockDim.x) cp_async16(&tile[swz(e)], &v[base | tab[e >> c] | (e & cmask)]);
+    if (fs) {  // fused QR: gather the tile from the source PEs, write to the spare buffer
+        std::uint64_t* words = tab + nt;
+        fused_tables(*fs, tab, nt, base, fs->pe_begin + t / tiles_per_pe, words);
+        for (int e = threadIdx.x; e < E; e += blockDim.x) cp_async16(&tile[swz(e)], fused_src(*fs, words, e, cmask, c));
+        v = fs->dst[t / tiles_per_pe];
+    } else {
+        for (int e = threadIdx.x; e < E; e += blockDim.x) cp_async16(&tile[swz(e)], &v[base | tab[e >> c] | (e & cmask)]);
+    }
     cp_async_wait_all();
     __syncthreads();
 
@@ -1340,24 +1348,45 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
         std::vector<double>& f;
         ~GiveBack() { frag_storage().swap(f); }
     } give_back{plan.frags};
+    // A pending QR is executed by the first pass (qrt_fused.h) unless that
+    // pass is an out-of-place wide gate.
+    bool fuse_first = false;
+    FusedSource fsrc{};
+    if (st->qr_pending) {
+        if (!hdrs.empty() && hdrs[0].T >= 0) {
+            fuse_first = true;
+            ensure_alt(st);
+            for (int pe = 0; pe < st->p; ++pe) fsrc.src[pe] = st->peer[st->cur][static_cast<std::size_t>(pe)];
+            for (int i = 0; i < st->pe_count; ++i) fsrc.dst[i] = st->bufs[st->cur ^ 1][static_cast<std::size_t>(i)];
+            for (int s2 = 0; s2 < st->n; ++s2) fsrc.src_of[st->qr_dest[static_cast<std::size_t>(s2)]] = s2;
+            fsrc.n = st->n;
+            fsrc.nl = st->nl;
+            fsrc.pe_begin = st->pe_begin;
+        } else {
+            flush_reorder(st);
+        }
+    }
     const std::size_t ops_bytes = dev_ops.size() * sizeof(GateOp);
     const std::size_t pool_off = (ops_bytes + 255) & ~std::size_t{255};
     const std::size_t pool_bytes = pool.size() * sizeof(double2);
     const std::size_t wpos_off = (pool_off + pool_bytes + 255) & ~std::size_t{255};
     const std::size_t frag_off = (wpos_off + wide_pos.size() * sizeof(int) + 255) & ~std::size_t{255};
-    const std::size_t total = frag_off + frags.size() * sizeof(double) + 16;
+    const std::size_t fs_off = (frag_off + frags.size() * sizeof(double) + 255) & ~std::size_t{255};
+    const std::size_t total = fs_off + sizeof(FusedSource) + 16;
     char* host = static_cast<char*>(ensure_pinned(st, total));
     QRT_CUDA(cudaStreamSynchronize(st->stream));  // pinned buffer may still feed a previous copy
     std::memcpy(host, dev_ops.data(), ops_bytes);
     std::memcpy(host + pool_off, pool.data(), pool_bytes);
     std::memcpy(host + wpos_off, wide_pos.data(), wide_pos.size() * sizeof(int));
     std::memcpy(host + frag_off, frags.data(), frags.size() * sizeof(double));
+    std::memcpy(host + fs_off, &fsrc, sizeof(FusedSource));
     char* dev = static_cast<char*>(ensure_ops(st, total));
     QRT_CUDA(cudaMemcpyAsync(dev, host, total, cudaMemcpyHostToDevice, st->stream));
     const GateOp* d_ops = reinterpret_cast<const GateOp*>(dev);
     const double2* d_pool = reinterpret_cast<const double2*>(dev + pool_off);
     const int* d_wpos = reinterpret_cast<const int*>(dev + wpos_off);
     const double* d_frags = reinterpret_cast<const double*>(dev + frag_off);
+    const FusedSource* d_fs = reinterpret_cast<const FusedSource*>(dev + fs_off);
 
     static bool attr_done[64] = {};
     if (!attr_done[st->device]) {
@@ -1370,10 +1399,16 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
     st->stats[QRT_K_GATES].flops += call_flops;
     for (std::size_t pi = 0; pi < hdrs.size(); ++pi) {
         const PassHdr& h = hdrs[pi];
+        const bool fused = fuse_first && pi == 0;
+        if (fused) barrier_on_stream(st);  // every source buffer complete on every rank
         if (h.T >= kLightMarker) {
             LightParams& L = *light[static_cast<std::size_t>(h.T - kLightMarker)];
             for (int i = 0; i < st->pe_count; ++i) L.ptrs[i] = st->live(i);
-            launch_light_pass(L, L.tiles_per_pe * st->pe_count, st->stream, st->device);
+            launch_light_pass(L, L.tiles_per_pe * st->pe_count, st->stream, st->device, fused ? d_fs : nullptr);
+            if (fused) {
+                st->cur ^= 1;
+                st->qr_pending = false;
+            }
             st->stats[QRT_K_GATES].launches++;
             st->stats[QRT_K_GATES].bytes += 32.0 * amps_all;
             continue;
@@ -1400,11 +1435,17 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
         std::copy(pmats[pi].begin(), pmats[pi].end(), params.mats);
         const int tiles = 1 << (st->nl - h.T);
         const int total_tiles = tiles * st->pe_count;
+        const std::size_t nt = static_cast<std::size_t>(1) << (h.T - h.c);
         const std::size_t smem = (static_cast<std::size_t>(1) << h.T) * sizeof(double2) +
                                  static_cast<std::size_t>(h.mat_count) * sizeof(double2) +
-                                 (static_cast<std::size_t>(1) << (h.T - h.c)) * sizeof(std::uint64_t);
-        gate_pass_kernel<<<total_tiles, gate_threads(), smem, st->stream>>>(params, d_pool, d_frags, tiles);
+                                 (nt + (fused ? kFusedSmemWords + nt : 0)) * sizeof(std::uint64_t);
+        gate_pass_kernel<<<total_tiles, gate_threads(), smem, st->stream>>>(params, d_pool, d_frags, tiles,
+                                                                            fused ? d_fs : nullptr);
         QRT_CUDA(cudaGetLastError());
+        if (fused) {
+            st->cur ^= 1;
+            st->qr_pending = false;
+        }
         st->stats[QRT_K_GATES].launches++;
         st->stats[QRT_K_GATES].bytes += 32.0 * amps_all;
     }

@@ -77,6 +77,11 @@ struct qrt_state {
     std::size_t pinned_cap = 0;
     int* d_flag = nullptr;  // barrier word for NCCL
 
+    // A QR recorded but not yet executed: the next gate pass gathers its tile
+    // through it (qrt_fused.h); any other access executes it first.
+    bool qr_pending = false;
+    std::vector<int> qr_dest;
+
     // Measurement.
     bool profile = false;
     qrt_kernel_stats stats[QRT_K_COUNT]{};
@@ -106,6 +111,8 @@ void barrier_on_stream(qrt_state* st);  // NCCL all-reduce of one int (no-op sin
 void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, const double* mats,
                  const unsigned* flags);
 std::uint64_t reorder(qrt_state* st, const int* dest);
+void flush_reorder(qrt_state* st);  // execute a pending QR (no-op if none)
+bool fused_qr_enabled();
 void reorder_plan(int n, int p, const int* dest, int src_pe, std::uint64_t* dst_pe, std::uint64_t* dst_off,
                   std::uint64_t* relocated);
 void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const std::uint64_t* y,

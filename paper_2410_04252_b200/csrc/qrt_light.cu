@@ -4,6 +4,7 @@
 // gate of the pass, in an order that never swaps two gates sharing a qubit.
 // One CTA = one 2^12-amplitude tile = 256 threads x 16 amplitudes.
 
+#include "qrt_fused.h"
 #include "qrt_light.h"
 
 namespace qrt {
@@ -122,7 +123,8 @@ __device__ __forceinline__ int diag_index(const LightOp& op, int f, int r) {
     return m;
 }
 
-__global__ void __launch_bounds__(kLightThreads, 2) light_pass_kernel(const __grid_constant__ LightParams P) {
+__global__ void __launch_bounds__(kLightThreads, 2)
+    light_pass_kernel(const __grid_constant__ LightParams P, const FusedSource* __restrict__ fs) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int E = 1 << kTileBits;
     double2* tile = reinterpret_cast<double2*>(smem_raw);
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(kLightThreads, 2) light_pass_kernel(const __gr
     amp_t* __restrict__ v = P.ptrs[blockIdx.x / P.tiles_per_pe];
     const int nt = 1 << (kTileBits - c);
     const int cmask = (1 << c) - 1;
-    if (!P.direct_in || !P.direct_out) {
+    if (!P.direct_in || !P.direct_out || fs) {
         for (int h = t; h < nt; h += kLightThreads) {
             u64 o = 0;
             for (int i = c; i < kTileBits; ++i) o |= static_cast<u64>((h >> (i - c)) & 1) << P.tile_pos[i];
@@ -144,6 +146,9 @@ __global__ void __launch_bounds__(kLightThreads, 2) light_pass_kernel(const __gr
         }
         __syncthreads();
     }
+    u64* fwords = tab + nt;  // fused QR tables (host sizes shared memory for them)
+    if (fs) fused_tables(*fs, tab, nt, cta, fs->pe_begin + static_cast<int>(blockIdx.x / P.tiles_per_pe), fwords);
+    amp_t* __restrict__ vout = fs ? fs->dst[blockIdx.x / P.tiles_per_pe] : v;
 
     double2 a[16];
     unsigned pend = 0;  // pending slot signs
@@ -174,7 +179,7 @@ __global__ void __launch_bounds__(kLightThreads, 2) light_pass_kernel(const __gr
 
     // ---- stage 0 input
     map_stage(P.st[0]);
-    if (P.direct_in) {
+    if (P.direct_in && !fs) {
         const u64 g0 = gofs(ebase);
         u64 gq[4];
 #pragma unroll
@@ -190,8 +195,8 @@ __global__ void __launch_bounds__(kLightThreads, 2) light_pass_kernel(const __gr
     } else {
         for (int e = t; e < E; e += kLightThreads) {
             const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&tile[swz(e)]));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
-                         "l"(&v[cta | tab[e >> c] | (e & cmask)]));
+            const amp_t* src = fs ? fused_src(*fs, fwords, e, cmask, c) : &v[cta | tab[e >> c] | (e & cmask)];
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src));
         }
         asm volatile("cp.async.wait_all;\n" ::);
         __syncthreads();
@@ -283,7 +288,7 @@ __global__ void __launch_bounds__(kLightThreads, 2) light_pass_kernel(const __gr
 #pragma unroll
             for (int q = 0; q < 4; ++q)
                 if ((r >> q) & 1) o |= gq[q];
-            __stcs(&v[o], a[r]);
+            __stcs(&vout[o], a[r]);
         }
     } else {
         const int sb = swz(ebase);
@@ -291,21 +296,22 @@ __global__ void __launch_bounds__(kLightThreads, 2) light_pass_kernel(const __gr
 #pragma unroll
         for (int r = 0; r < 16; ++r) tile[sslot(sb, r)] = a[r];
         __syncthreads();
-        for (int e = t; e < E; e += kLightThreads) __stcs(&v[cta | tab[e >> c] | (e & cmask)], tile[swz(e)]);
+        for (int e = t; e < E; e += kLightThreads) __stcs(&vout[cta | tab[e >> c] | (e & cmask)], tile[swz(e)]);
     }
 }
 
 }  // namespace
 
-void launch_light_pass(const LightParams& P, int total_tiles, cudaStream_t stream, int device) {
+void launch_light_pass(const LightParams& P, int total_tiles, cudaStream_t stream, int device, const FusedSource* fs) {
     static bool attr_done[64] = {};
+    const std::size_t nt = std::size_t{1} << (kTileBits - P.c);
     const std::size_t smem = (std::size_t{1} << kTileBits) * sizeof(double2) +
-                             (std::size_t{1} << (kTileBits - P.c)) * sizeof(std::uint64_t);
+                             (nt + (fs ? kFusedSmemWords + nt : 0)) * sizeof(std::uint64_t);
     if (!attr_done[device]) {
         QRT_CUDA(cudaFuncSetAttribute(light_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
         attr_done[device] = true;
     }
-    light_pass_kernel<<<total_tiles, kLightThreads, smem, stream>>>(P);
+    light_pass_kernel<<<total_tiles, kLightThreads, smem, stream>>>(P, fs);
     QRT_CUDA(cudaGetLastError());
 }
 

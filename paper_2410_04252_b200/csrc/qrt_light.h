@@ -87,6 +87,8 @@ struct LightParams {
     double2 mats[kLightMaxMats];
 };
 
-void launch_light_pass(const LightParams& P, int total_tiles, cudaStream_t stream, int device);
+struct FusedSource;
+void launch_light_pass(const LightParams& P, int total_tiles, cudaStream_t stream, int device,
+                       const FusedSource* fs = nullptr);
 
 }  // namespace qrt

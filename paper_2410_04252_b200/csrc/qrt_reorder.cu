@@ -19,6 +19,7 @@
 // query qrt_reorder_plan, which the CPU multi-process tests use to emulate
 // the exchange exactly.
 
+#include <cstdlib>
 #include <numeric>
 
 #include "qrt_internal.h"
@@ -178,11 +179,23 @@ std::uint64_t build_map(int n, int nl, int pe_begin, const int* dest, QrMap& a, 
 
 }  // namespace
 
-std::uint64_t reorder(qrt_state* st, const int* dest) {
+bool fused_qr_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("QRT_FUSED_QR");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    return on;
+}
+
+namespace {
+
+// The push exchange: every PE stores its amplitudes into the spare buffer of
+// the destination PE, then all ranks meet and flip buffers.
+void execute_reorder(qrt_state* st, const int* dest) {
     QrArgs a{};
     bool identity = false;
     const std::uint64_t relocated = build_map(st->n, st->nl, st->pe_begin, dest, a.m, identity);
-    if (identity) return 0;
+    if (identity) return;
     if (st->p > kMaxLocalPEs) fail(QRT_ERR_CONFIG, "too many PEs for the reorder kernel");
     ensure_alt(st);
     const int nxt = st->cur ^ 1;
@@ -190,6 +203,7 @@ std::uint64_t reorder(qrt_state* st, const int* dest) {
     for (int i = 0; i < st->pe_count; ++i) a.src[i] = st->live(i);
     {
         ProfileScope prof(st, QRT_K_QR);
+        barrier_on_stream(st);  // no peer still reads the buffers written here (fused passes)
         dim3 grid(static_cast<unsigned>(1ull << a.m.n_hi), static_cast<unsigned>(st->pe_count));
         reorder_kernel<<<grid, 256, 0, st->stream>>>(a);
         QRT_CUDA(cudaGetLastError());
@@ -199,7 +213,29 @@ std::uint64_t reorder(qrt_state* st, const int* dest) {
     // bytes that cross to another PE (each way), counted for this process's PEs
     st->stats[QRT_K_QR].bytes += 16.0 * static_cast<double>(relocated) * st->pe_count / st->p;
     st->cur = nxt;
+}
+
+}  // namespace
+
+std::uint64_t reorder(qrt_state* st, const int* dest) {
+    QrMap m{};
+    bool identity = false;
+    const std::uint64_t relocated = build_map(st->n, st->nl, st->pe_begin, dest, m, identity);
+    if (identity) return 0;
+    flush_reorder(st);
+    if (fused_qr_enabled() && st->p > 1) {
+        st->qr_pending = true;  // the next gate pass gathers through it
+        st->qr_dest.assign(dest, dest + st->n);
+        return relocated;
+    }
+    execute_reorder(st, dest);
     return relocated;
+}
+
+void flush_reorder(qrt_state* st) {
+    if (!st->qr_pending) return;
+    st->qr_pending = false;
+    execute_reorder(st, st->qr_dest.data());
 }
 
 // Host-side replay of the kernel's index mapping for one source PE: for every

@@ -223,7 +223,15 @@ std::uint64_t reorder(qrt_state* st, const int* dest) {
     const std::uint64_t relocated = build_map(st->n, st->nl, st->pe_begin, dest, m, identity);
     if (identity) return 0;
     flush_reorder(st);
-    if (fused_qr_enabled() && st->p > 1) {
+    // Pulling a tile's sources over NVLink scatters each CTA's reads over the
+    // whole peer buffer; past 2^30 amplitudes (16 GiB) per PE the translation
+    // misses outweigh the saved exchange (34-qubit HEA on 4 GPUs: 0.31 s
+    // slower), so large states keep the push exchange.
+    static const int max_log2 = [] {
+        const char* e = std::getenv("QRT_FUSED_QR_MAX_LOG2");
+        return e ? std::atoi(e) : 30;
+    }();
+    if (fused_qr_enabled() && st->p > 1 && st->nl <= max_log2) {
         st->qr_pending = true;  // the next gate pass gathers through it
         st->qr_dest.assign(dest, dest + st->n);
         return relocated;

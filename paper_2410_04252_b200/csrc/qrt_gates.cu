@@ -322,9 +322,11 @@ __device__ __forceinline__ void diagonal(double2* __restrict__ tile, const doubl
 // One CTA per tile; several CTAs per SM so one CTA's load / store phase
 // overlaps another's fp64 math.  The pass's DMMA B fragments are read
 // through L1 (they are shared by every CTA of the pass).
+template <bool FUSED>  // FUSED: gather the tile through a pending QR (qrt_fused.h)
 __global__ void __launch_bounds__(256, 2)
     gate_pass_kernel(const __grid_constant__ PassParams P, const double2* __restrict__ pool,
-                     const double* __restrict__ frags, int tiles_per_pe, const FusedSource* __restrict__ fs) {
+                     const double* __restrict__ frags, int tiles_per_pe, const FusedSource* __restrict__ fs_arg) {
+    const FusedSource* __restrict__ fs = FUSED ? fs_arg : nullptr;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const PassHdr& hdr = P.hdr;
     const int T = hdr.T, E = 1 << T, c = hdr.c;
@@ -1390,7 +1392,8 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
 
     static bool attr_done[64] = {};
     if (!attr_done[st->device]) {
-        QRT_CUDA(cudaFuncSetAttribute(gate_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        QRT_CUDA(cudaFuncSetAttribute(gate_pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        QRT_CUDA(cudaFuncSetAttribute(gate_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr_done[st->device] = true;
     }
 
@@ -1439,8 +1442,11 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
         const std::size_t smem = (static_cast<std::size_t>(1) << h.T) * sizeof(double2) +
                                  static_cast<std::size_t>(h.mat_count) * sizeof(double2) +
                                  (nt + (fused ? kFusedSmemWords + nt : 0)) * sizeof(std::uint64_t);
-        gate_pass_kernel<<<total_tiles, gate_threads(), smem, st->stream>>>(params, d_pool, d_frags, tiles,
-                                                                            fused ? d_fs : nullptr);
+        if (fused)
+            gate_pass_kernel<true><<<total_tiles, gate_threads(), smem, st->stream>>>(params, d_pool, d_frags, tiles, d_fs);
+        else
+            gate_pass_kernel<false><<<total_tiles, gate_threads(), smem, st->stream>>>(params, d_pool, d_frags, tiles,
+                                                                                     nullptr);
         QRT_CUDA(cudaGetLastError());
         if (fused) {
             st->cur ^= 1;

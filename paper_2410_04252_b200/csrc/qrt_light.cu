@@ -123,8 +123,12 @@ __device__ __forceinline__ int diag_index(const LightOp& op, int f, int r) {
     return m;
 }
 
+// FUSED: the pass gathers its tile through a pending QR (qrt_fused.h); a
+// separate instantiation so the common path carries no extra registers.
+template <bool FUSED>
 __global__ void __launch_bounds__(kLightThreads, 2)
-    light_pass_kernel(const __grid_constant__ LightParams P, const FusedSource* __restrict__ fs) {
+    light_pass_kernel(const __grid_constant__ LightParams P, const FusedSource* __restrict__ fs_arg) {
+    const FusedSource* __restrict__ fs = FUSED ? fs_arg : nullptr;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int E = 1 << kTileBits;
     double2* tile = reinterpret_cast<double2*>(smem_raw);
@@ -179,7 +183,7 @@ __global__ void __launch_bounds__(kLightThreads, 2)
 
     // ---- stage 0 input
     map_stage(P.st[0]);
-    if (P.direct_in && !fs) {
+    if (P.direct_in && !FUSED) {
         const u64 g0 = gofs(ebase);
         u64 gq[4];
 #pragma unroll
@@ -308,10 +312,14 @@ void launch_light_pass(const LightParams& P, int total_tiles, cudaStream_t strea
     const std::size_t smem = (std::size_t{1} << kTileBits) * sizeof(double2) +
                              (nt + (fs ? kFusedSmemWords + nt : 0)) * sizeof(std::uint64_t);
     if (!attr_done[device]) {
-        QRT_CUDA(cudaFuncSetAttribute(light_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        QRT_CUDA(cudaFuncSetAttribute(light_pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        QRT_CUDA(cudaFuncSetAttribute(light_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
         attr_done[device] = true;
     }
-    light_pass_kernel<<<total_tiles, kLightThreads, smem, stream>>>(P, fs);
+    if (fs)
+        light_pass_kernel<true><<<total_tiles, kLightThreads, smem, stream>>>(P, fs);
+    else
+        light_pass_kernel<false><<<total_tiles, kLightThreads, smem, stream>>>(P, nullptr);
     QRT_CUDA(cudaGetLastError());
 }
 

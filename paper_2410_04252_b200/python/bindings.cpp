@@ -191,7 +191,10 @@ PYBIND11_MODULE(_qrtile, m) {
         .def_readonly("inter", &QrCounts::inter);
     py::class_<CostWeights>(m, "CostWeights")
         .def(py::init([](double a, double b) { return CostWeights{a, b}; }), py::arg("w_intra") = 1.0,
-             py::arg("w_inter") = 24.0);
+             py::arg("w_inter") = 24.0)
+        .def_readwrite("w_intra", &CostWeights::w_intra)
+        .def_readwrite("w_inter", &CostWeights::w_inter)
+        .def("validate", &CostWeights::validate);
 
     m.def("flat_tiling", &flat_tiling);
     m.def("hierarchical_tiling", &hierarchical_tiling);

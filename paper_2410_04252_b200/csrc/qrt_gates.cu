@@ -64,6 +64,7 @@ struct PassHdr {
     int frag_begin;      // first double of this pass's DMMA B fragments in the fragment pool
     int frag_count;
     int n_outer;
+    int gauss;           // DMMA gates use the 3-product (Gauss) complex form, see dense_gauss
     int tile_pos[kTileBits];
     int outer_pos[64];
 };
@@ -250,6 +251,93 @@ __device__ __forceinline__ void dense_dmma(double2* __restrict__ tile, const dou
     }
 }
 
+// Dense k = 3, 4 on DMMA with the 3-multiplication complex product (Gauss):
+// for U = X + iY and amplitudes a = p + iq,
+//   k1 = X (p + q),  k2 = (Y - X) p,  k3 = (X + Y) q,   Re = k1 - k3,  Im = k1 + k2,
+// i.e. three real D x D products instead of the one 2D x 2D real form
+// (24 instead of 32 DMMA.8x8x4 per 8 groups at k = 4), plus 3 DADDs per
+// amplitude on the same fp64 pipe.  A fragments: lane holds amplitude
+// c = 4 kb + (lane & 3) of group lane >> 2 (one 16-byte load gives p and q);
+// C fragments: output amplitudes 8 nb + 2 (lane & 3) + {0, 1}.  B fragment
+// slot ((t * NB + nb) * KB + kb) * 32 + lane holds M_t[n][k] with
+// k = 4 kb + (lane & 3), n = 8 nb + (lane >> 2), M_0 = X, M_1 = Y - X, M_2 = X + Y.
+template <int K>
+__device__ __forceinline__ void dense_gauss(double2* __restrict__ tile, const double* __restrict__ frag,
+                                            const GateOp& op, int E) {
+    constexpr int D = 1 << K, NB = D / 8, KB = D / 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    int tb[K], sb[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) sb[j] = tb[j] = op.tb[j];
+#pragma unroll
+    for (int a = 1; a < K; ++a)
+#pragma unroll
+        for (int q = K - 1; q >= a; --q)
+            if (sb[q - 1] > sb[q]) {
+                const int t = sb[q];
+                sb[q] = sb[q - 1];
+                sb[q - 1] = t;
+            }
+    auto spread = [&](int m) {
+        int o = 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) o |= ((m >> j) & 1) << tb[j];
+        return o;
+    };
+    int sa[KB], sc[NB][2];
+#pragma unroll
+    for (int kb = 0; kb < KB; ++kb) sa[kb] = swz(spread(4 * kb + (lane & 3)));
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+        sc[nb][0] = swz(spread(8 * nb + 2 * (lane & 3)));
+        sc[nb][1] = swz(spread(8 * nb + 2 * (lane & 3) + 1));
+    }
+    const double* __restrict__ fl = frag + lane;
+    const int blocks = (E >> K) >> 3;
+    auto row_base = [&](int rb) {
+        int base = rb * 8 + (lane >> 2);
+#pragma unroll
+        for (int j = 0; j < K; ++j) base = insert_zero(base, sb[j]);
+        return swz(base);
+    };
+    for (int rb = warp; rb < blocks; rb += 2 * nwarps) {
+        const int rb1 = rb + nwarps;
+        const bool two = rb1 < blocks;
+        const int s0 = row_base(rb), s1 = two ? row_base(rb1) : s0;
+        double c0[3][NB][2], c1[3][NB][2];
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) c0[t][nb][0] = c0[t][nb][1] = c1[t][nb][0] = c1[t][nb][1] = 0.0;
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) {
+            const double2 x0 = tile[s0 ^ sa[kb]], x1 = tile[s1 ^ sa[kb]];
+            const double a0[3] = {x0.x + x0.y, x0.x, x0.y};
+            const double a1[3] = {x1.x + x1.y, x1.x, x1.y};
+#pragma unroll
+            for (int t = 0; t < 3; ++t)
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb) {
+                    const double b = fl[((t * NB + nb) * KB + kb) * 32];
+                    dmma_8x8x4(c0[t][nb][0], c0[t][nb][1], a0[t], b);
+                    dmma_8x8x4(c1[t][nb][0], c1[t][nb][1], a1[t], b);
+                }
+        }
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+                tile[s0 ^ sc[nb][j]] = make_double2(c0[0][nb][j] - c0[2][nb][j], c0[0][nb][j] + c0[1][nb][j]);
+        if (two) {
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+                    tile[s1 ^ sc[nb][j]] = make_double2(c1[0][nb][j] - c1[2][nb][j], c1[0][nb][j] + c1[1][nb][j]);
+        }
+    }
+}
+
 // Dense 5 <= k <= 7: one warp per group, lanes split the rows.
 __device__ __forceinline__ void dense_wide(double2* __restrict__ tile, const double2* __restrict__ u,
                                            const GateOp& op, int E) {
@@ -373,13 +461,17 @@ __global__ void __launch_bounds__(256, 2)
                 case 1: dense_small<1>(tile, P, pm, op, E); break;
                 case 2: dense_small<2>(tile, P, pm, op, E); break;
                 case 3:
-                    if (op.bfrag >= 0)
+                    if (op.bfrag >= 0 && hdr.gauss)
+                        dense_gauss<3>(tile, pf + op.bfrag, op, E);
+                    else if (op.bfrag >= 0)
                         dense_dmma<3>(tile, pf + op.bfrag, op, E);
                     else
                         dense_small<3>(tile, P, pm, op, E);
                     break;
                 case 4:
-                    if (op.bfrag >= 0)
+                    if (op.bfrag >= 0 && hdr.gauss)
+                        dense_gauss<4>(tile, pf + op.bfrag, op, E);
+                    else if (op.bfrag >= 0)
                         dense_dmma<4>(tile, pf + op.bfrag, op, E);
                     else
                         dense_small<4>(tile, P, pm, op, E);
@@ -568,6 +660,30 @@ std::vector<std::pair<int, double>> frag_map(int k) {
                     m.emplace_back(at + 1, i == 0 ? -1.0 : 1.0);  // -Im / +Im
             }
     return m;
+}
+
+// Gauss form (see dense_gauss): slot ((t * NB + nb) * KB + kb) * 32 + lane
+// holds M_t[n][k], k = 4 kb + (lane & 3), n = 8 nb + (lane >> 2), with
+// M_0 = Re U, M_1 = Im U - Re U, M_2 = Re U + Im U.
+void gauss_frags(int k, const double* m, double* dst) {
+    const int D = 1 << k, NB = D / 8, KB = D / 4;
+    for (int t = 0; t < 3; ++t)
+        for (int nb = 0; nb < NB; ++nb)
+            for (int kb = 0; kb < KB; ++kb)
+                for (int lane = 0; lane < 32; ++lane) {
+                    const int kk = 4 * kb + (lane & 3), nn = 8 * nb + (lane >> 2);
+                    const double x = m[2 * (nn * D + kk)], y = m[2 * (nn * D + kk) + 1];
+                    *dst++ = t == 0 ? x : t == 1 ? y - x : x + y;
+                }
+}
+
+// DMMA gates in the Gauss form (QRT_GAUSS=0: the 2D x 2D real form).
+bool gauss_mode() {
+    static const bool v = [] {
+        const char* e = std::getenv("QRT_GAUSS");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    return v;
 }
 
 // Per-thread storage recycled between calls for the DMMA fragment pool.
@@ -1062,7 +1178,8 @@ GatePlan plan_gates(int nl, int n_gates, const int* arity, const int* pos, const
             if (!ps.light && !ps.wide)
                 for (int id : ps.ops) {
                     const HostOp& o = opsv[static_cast<std::size_t>(id)];
-                    if (o.kind == kDense && (o.k == 3 || o.k == 4) && ps.T >= o.k + 3) need += 4u * o.mat_len;
+                    if (o.kind == kDense && (o.k == 3 || o.k == 4) && ps.T >= o.k + 3)
+                        need += (gauss_mode() ? 3u : 4u) * o.mat_len;
                 }
         frags.reserve(need);
     }
@@ -1285,6 +1402,7 @@ GatePlan plan_gates(int nl, int n_gates, const int* arity, const int* pos, const
         };
         int staged = 0;
         h.frag_begin = static_cast<int>(frags.size());
+        h.gauss = gauss_mode() ? 1 : 0;
         std::vector<std::pair<int, int>> late;  // (op index in dev_ops, host op)
         for (int id : ps.ops) {
             const HostOp& o = opsv[static_cast<std::size_t>(id)];
@@ -1309,9 +1427,14 @@ GatePlan plan_gates(int nl, int n_gates, const int* arity, const int* pos, const
                 static const std::vector<std::pair<int, double>> map3 = frag_map(3), map4 = frag_map(4);
                 const auto& fm = o.k == 3 ? map3 : map4;
                 const std::size_t at = frags.size();
-                frags.resize(at + static_cast<std::size_t>(R) * R);
-                double* dst = frags.data() + at;
-                for (std::size_t e = 0; e < fm.size(); ++e) dst[e] = fm[e].second * o.m[fm[e].first];
+                if (h.gauss) {
+                    frags.resize(at + 3u * static_cast<std::size_t>(D) * D);
+                    gauss_frags(o.k, o.m, frags.data() + at);
+                } else {
+                    frags.resize(at + static_cast<std::size_t>(R) * R);
+                    double* dst = frags.data() + at;
+                    for (std::size_t e = 0; e < fm.size(); ++e) dst[e] = fm[e].second * o.m[fm[e].first];
+                }
             } else if (o.k <= 4) {
                 g.pmat = static_cast<int>(pmats[pidx].size());
                 put(pmats[pidx], o);

@@ -172,6 +172,13 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                  : "d"(a), "d"(b));
 }
 
+// D = A B + C with a separate accumulator input.
+__device__ __forceinline__ void dmma_8x8x4_c(double& d0, double& d1, double a, double b, double c0, double c1) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+                 : "=d"(d0), "=d"(d1)
+                 : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
+
 // Dense k = 3, 4 on the FP64 tensor path (DMMA, m8n8k4): for 8 groups at a
 // time, OUT[8 x 2D] = IN[8 x 2D] * M^T where M is the 2D x 2D real form of U
 // ([[Re, -Im], [Im, Re]] blocks) — the interleaved (re, im) amplitude layout
@@ -253,14 +260,16 @@ __device__ __forceinline__ void dense_dmma(double2* __restrict__ tile, const dou
 
 // Dense k = 3, 4 on DMMA with the 3-multiplication complex product (Gauss):
 // for U = X + iY and amplitudes a = p + iq,
-//   k1 = X (p + q),  k2 = (Y - X) p,  k3 = (X + Y) q,   Re = k1 - k3,  Im = k1 + k2,
+//   k1 = X (p + q),  Re = k1 + (-(X + Y)) q,  Im = k1 + (Y - X) p,
 // i.e. three real D x D products instead of the one 2D x 2D real form
-// (24 instead of 32 DMMA.8x8x4 per 8 groups at k = 4), plus 3 DADDs per
-// amplitude on the same fp64 pipe.  A fragments: lane holds amplitude
+// (24 instead of 32 DMMA.8x8x4 per 8 groups at k = 4); the Re / Im chains
+// start from k1 as their accumulator input, so the only DADD left is p + q
+// (one per amplitude; DMMA and DADD share the fp64 datapath, measured:
+// tools/microbench_fp64.cu).  A fragments: lane holds amplitude
 // c = 4 kb + (lane & 3) of group lane >> 2 (one 16-byte load gives p and q);
 // C fragments: output amplitudes 8 nb + 2 (lane & 3) + {0, 1}.  B fragment
 // slot ((t * NB + nb) * KB + kb) * 32 + lane holds M_t[n][k] with
-// k = 4 kb + (lane & 3), n = 8 nb + (lane >> 2), M_0 = X, M_1 = Y - X, M_2 = X + Y.
+// k = 4 kb + (lane & 3), n = 8 nb + (lane >> 2), M_0 = X, M_1 = Y - X, M_2 = -(X + Y).
 template <int K>
 __device__ __forceinline__ void dense_gauss(double2* __restrict__ tile, const double* __restrict__ frag,
                                             const GateOp& op, int E) {
@@ -304,36 +313,51 @@ __device__ __forceinline__ void dense_gauss(double2* __restrict__ tile, const do
         const int rb1 = rb + nwarps;
         const bool two = rb1 < blocks;
         const int s0 = row_base(rb), s1 = two ? row_base(rb1) : s0;
-        double c0[3][NB][2], c1[3][NB][2];
+        // k1 = X (p + q) first; Re and Im chains then start from k1 as the
+        // DMMA accumulator input, so the output needs no DADDs.
+        double2 x0[KB], x1[KB];
+        double k0[NB][2], k1[NB][2];
 #pragma unroll
-        for (int t = 0; t < 3; ++t)
-#pragma unroll
-            for (int nb = 0; nb < NB; ++nb) c0[t][nb][0] = c0[t][nb][1] = c1[t][nb][0] = c1[t][nb][1] = 0.0;
+        for (int nb = 0; nb < NB; ++nb) k0[nb][0] = k0[nb][1] = k1[nb][0] = k1[nb][1] = 0.0;
 #pragma unroll
         for (int kb = 0; kb < KB; ++kb) {
-            const double2 x0 = tile[s0 ^ sa[kb]], x1 = tile[s1 ^ sa[kb]];
-            const double a0[3] = {x0.x + x0.y, x0.x, x0.y};
-            const double a1[3] = {x1.x + x1.y, x1.x, x1.y};
+            x0[kb] = tile[s0 ^ sa[kb]];
+            x1[kb] = tile[s1 ^ sa[kb]];
+            const double a0 = x0[kb].x + x0[kb].y, a1 = x1[kb].x + x1[kb].y;
 #pragma unroll
-            for (int t = 0; t < 3; ++t)
-#pragma unroll
-                for (int nb = 0; nb < NB; ++nb) {
-                    const double b = fl[((t * NB + nb) * KB + kb) * 32];
-                    dmma_8x8x4(c0[t][nb][0], c0[t][nb][1], a0[t], b);
-                    dmma_8x8x4(c1[t][nb][0], c1[t][nb][1], a1[t], b);
-                }
+            for (int nb = 0; nb < NB; ++nb) {
+                const double b = fl[(nb * KB + kb) * 32];
+                dmma_8x8x4(k0[nb][0], k0[nb][1], a0, b);
+                dmma_8x8x4(k1[nb][0], k1[nb][1], a1, b);
+            }
         }
+        double re0[NB][2], im0[NB][2], re1[NB][2], im1[NB][2];
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb)
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) {
+                const double bi = fl[((NB + nb) * KB + kb) * 32], br = fl[((2 * NB + nb) * KB + kb) * 32];
+                if (kb == 0) {
+                    dmma_8x8x4_c(re0[nb][0], re0[nb][1], x0[0].y, br, k0[nb][0], k0[nb][1]);
+                    dmma_8x8x4_c(re1[nb][0], re1[nb][1], x1[0].y, br, k1[nb][0], k1[nb][1]);
+                    dmma_8x8x4_c(im0[nb][0], im0[nb][1], x0[0].x, bi, k0[nb][0], k0[nb][1]);
+                    dmma_8x8x4_c(im1[nb][0], im1[nb][1], x1[0].x, bi, k1[nb][0], k1[nb][1]);
+                } else {
+                    dmma_8x8x4(re0[nb][0], re0[nb][1], x0[kb].y, br);
+                    dmma_8x8x4(re1[nb][0], re1[nb][1], x1[kb].y, br);
+                    dmma_8x8x4(im0[nb][0], im0[nb][1], x0[kb].x, bi);
+                    dmma_8x8x4(im1[nb][0], im1[nb][1], x1[kb].x, bi);
+                }
+            }
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
-                tile[s0 ^ sc[nb][j]] = make_double2(c0[0][nb][j] - c0[2][nb][j], c0[0][nb][j] + c0[1][nb][j]);
+            for (int j = 0; j < 2; ++j) tile[s0 ^ sc[nb][j]] = make_double2(re0[nb][j], im0[nb][j]);
         if (two) {
 #pragma unroll
             for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-                for (int j = 0; j < 2; ++j)
-                    tile[s1 ^ sc[nb][j]] = make_double2(c1[0][nb][j] - c1[2][nb][j], c1[0][nb][j] + c1[1][nb][j]);
+                for (int j = 0; j < 2; ++j) tile[s1 ^ sc[nb][j]] = make_double2(re1[nb][j], im1[nb][j]);
         }
     }
 }
@@ -410,8 +434,10 @@ __device__ __forceinline__ void diagonal(double2* __restrict__ tile, const doubl
 // One CTA per tile; several CTAs per SM so one CTA's load / store phase
 // overlaps another's fp64 math.  The pass's DMMA B fragments are read
 // through L1 (they are shared by every CTA of the pass).
-template <bool FUSED>  // FUSED: gather the tile through a pending QR (qrt_fused.h)
-__global__ void __launch_bounds__(256, 2)
+// FUSED: gather the tile through a pending QR (qrt_fused.h).  MINB: CTAs per
+// SM the register budget is cut for (3: <= 168 registers, 4: <= 128).
+template <bool FUSED, int MINB>
+__global__ void __launch_bounds__(128, MINB)
     gate_pass_kernel(const __grid_constant__ PassParams P, const double2* __restrict__ pool,
                      const double* __restrict__ frags, int tiles_per_pe, const FusedSource* __restrict__ fs_arg) {
     const FusedSource* __restrict__ fs = FUSED ? fs_arg : nullptr;
@@ -513,13 +539,33 @@ __global__ void wide_gate_kernel(const amp_t* __restrict__ in, amp_t* __restrict
     }
 }
 
-// CTA size of the gate pass kernel: 128 (3 CTAs / SM) or 256 (2 CTAs / SM);
+// CTA size of the gate pass kernel: 128 (3 CTAs / SM, the launch bound) or 64;
 // QRT_GATE_THREADS overrides for experiments.
 int gate_threads() {
     static int v = [] {
         const char* e = std::getenv("QRT_GATE_THREADS");
         const int t = e ? std::atoi(e) : 128;
-        return (t == 256 || t == 128 || t == 64) ? t : 128;
+        return t == 64 ? 64 : 128;
+    }();
+    return v;
+}
+
+// Register budget of the gate pass kernel: the 4-CTA launch bound (<= 128
+// registers, measured fastest); QRT_GATE_REGS=168 selects the 3-CTA bound.
+int gate_minb() {
+    static const int v = [] {
+        const char* e = std::getenv("QRT_GATE_REGS");
+        return e && std::atoi(e) == 168 ? 3 : 4;
+    }();
+    return v;
+}
+
+// Low positions every shared-memory gate pass starts from (its HBM runs are
+// at least 2^c amplitudes); QRT_GATE_COAL overrides (0..4).
+int gate_coal_bits() {
+    static const int v = [] {
+        const char* e = std::getenv("QRT_GATE_COAL");
+        return e ? std::max(0, std::min(kCoalBits, std::atoi(e))) : kCoalBits;
     }();
     return v;
 }
@@ -664,7 +710,7 @@ std::vector<std::pair<int, double>> frag_map(int k) {
 
 // Gauss form (see dense_gauss): slot ((t * NB + nb) * KB + kb) * 32 + lane
 // holds M_t[n][k], k = 4 kb + (lane & 3), n = 8 nb + (lane >> 2), with
-// M_0 = Re U, M_1 = Im U - Re U, M_2 = Re U + Im U.
+// M_0 = Re U, M_1 = Im U - Re U, M_2 = -(Re U + Im U).
 void gauss_frags(int k, const double* m, double* dst) {
     const int D = 1 << k, NB = D / 8, KB = D / 4;
     for (int t = 0; t < 3; ++t)
@@ -673,15 +719,16 @@ void gauss_frags(int k, const double* m, double* dst) {
                 for (int lane = 0; lane < 32; ++lane) {
                     const int kk = 4 * kb + (lane & 3), nn = 8 * nb + (lane >> 2);
                     const double x = m[2 * (nn * D + kk)], y = m[2 * (nn * D + kk) + 1];
-                    *dst++ = t == 0 ? x : t == 1 ? y - x : x + y;
+                    *dst++ = t == 0 ? x : t == 1 ? y - x : -(x + y);
                 }
 }
 
-// DMMA gates in the Gauss form (QRT_GAUSS=0: the 2D x 2D real form).
-bool gauss_mode() {
-    static const bool v = [] {
+// DMMA gates in the Gauss form (dense_gauss; QRT_GAUSS=0: the 2D x 2D real
+// form, dense_dmma).
+int gauss_mode() {
+    static const int v = [] {
         const char* e = std::getenv("QRT_GAUSS");
-        return e ? std::atoi(e) != 0 : true;
+        return e ? std::atoi(e) : 1;
     }();
     return v;
 }
@@ -1048,7 +1095,7 @@ GatePlan plan_gates(int nl, int n_gates, const int* arity, const int* pos, const
                 const bool dmma = h.kind == kDense && (h.k == 3 || h.k == 4) && T_here >= h.k + 3;
                 const int in_params = (h.kind == kDense && h.k <= 4 && !dmma) ? h.mat_len : 0;
                 const int in_smem = h.kind == kDiag ? h.mat_len : 0;
-                const int in_frag = dmma ? 4 * h.mat_len : 0;  // (2D)^2 real entries
+                const int in_frag = dmma ? (gauss_mode() ? 3 : 4) * h.mat_len : 0;  // (2D)^2 real entries
                 ok = param_used + in_params <= kParamMats && diag_used + in_smem <= kDiagStage &&
                      frag_used + in_frag <= kFragStage && n < kMaxPassOps;
                 if (ok) {
@@ -1104,7 +1151,7 @@ GatePlan plan_gates(int nl, int n_gates, const int* arity, const int* pos, const
     // follow the light cone of the circuit instead of the first layer only.
     constexpr int kSeeds = 16;
     auto candidate = [&](std::size_t seed) {
-        std::uint64_t B = (1ull << kCoalBits) - 1, blocked = 0;
+        std::uint64_t B = (1ull << gate_coal_bits()) - 1, blocked = 0;
         const std::size_t m = remaining.size();
         for (std::size_t q = 0; q < m; ++q) {
             const HostOp& h = opsv[static_cast<std::size_t>(remaining[(seed + q) % m])];
@@ -1402,7 +1449,7 @@ GatePlan plan_gates(int nl, int n_gates, const int* arity, const int* pos, const
         };
         int staged = 0;
         h.frag_begin = static_cast<int>(frags.size());
-        h.gauss = gauss_mode() ? 1 : 0;
+        h.gauss = gauss_mode();
         std::vector<std::pair<int, int>> late;  // (op index in dev_ops, host op)
         for (int id : ps.ops) {
             const HostOp& o = opsv[static_cast<std::size_t>(id)];
@@ -1515,8 +1562,10 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
 
     static bool attr_done[64] = {};
     if (!attr_done[st->device]) {
-        QRT_CUDA(cudaFuncSetAttribute(gate_pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        QRT_CUDA(cudaFuncSetAttribute(gate_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        QRT_CUDA(cudaFuncSetAttribute(gate_pass_kernel<false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        QRT_CUDA(cudaFuncSetAttribute(gate_pass_kernel<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        QRT_CUDA(cudaFuncSetAttribute(gate_pass_kernel<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        QRT_CUDA(cudaFuncSetAttribute(gate_pass_kernel<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr_done[st->device] = true;
     }
 
@@ -1565,11 +1614,9 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
         const std::size_t smem = (static_cast<std::size_t>(1) << h.T) * sizeof(double2) +
                                  static_cast<std::size_t>(h.mat_count) * sizeof(double2) +
                                  (nt + (fused ? kFusedSmemWords + nt : 0)) * sizeof(std::uint64_t);
-        if (fused)
-            gate_pass_kernel<true><<<total_tiles, gate_threads(), smem, st->stream>>>(params, d_pool, d_frags, tiles, d_fs);
-        else
-            gate_pass_kernel<false><<<total_tiles, gate_threads(), smem, st->stream>>>(params, d_pool, d_frags, tiles,
-                                                                                     nullptr);
+        auto kern = fused ? (gate_minb() == 4 ? gate_pass_kernel<true, 4> : gate_pass_kernel<true, 3>)
+                          : (gate_minb() == 4 ? gate_pass_kernel<false, 4> : gate_pass_kernel<false, 3>);
+        kern<<<total_tiles, gate_threads(), smem, st->stream>>>(params, d_pool, d_frags, tiles, fused ? d_fs : nullptr);
         QRT_CUDA(cudaGetLastError());
         if (fused) {
             st->cur ^= 1;

@@ -84,7 +84,7 @@ def test_coset_deterministic(qb, device):
     assert e[0] == e[1] == e[2]
 
 
-@pytest.mark.parametrize("env", [{"QRT_EVC_GLOBAL_COVER": "0"}, {"QRT_COSET_OCC": "3"}, {"QRT_GATE_THREADS": "256"},
+@pytest.mark.parametrize("env", [{"QRT_EVC_GLOBAL_COVER": "0"}, {"QRT_COSET_OCC": "3"}, {"QRT_GATE_THREADS": "64"},
                                  {"QRT_PLAN_CACHE": "0"}, {"QRT_GAUSS": "0"}])
 def test_knobs_in_subprocess(env):
     """Knobs read once per process: a fresh process per setting, checked

@@ -332,6 +332,14 @@ def run_ours(args):
         # dense 4-qubit blocks on the fp64 tensor pipe: flop-bound (SURVEY.md section 7 hard parts)
         roof = {"bound": "tensor", "achieved": f["fp64_tflops_ref_equiv"], "peak": FP64_TENSOR_PEAK, "unit": "TFLOP/s",
                 "frac": f["fp64_frac"], "peak_kind": "measured fp64 DMMA (tools/microbench_fp64.cu)"}
+        # `achieved` counts the reference's algorithmic flops.  The Gauss-form
+        # kernel executes 3 real 16x16 products + 1 DADD per amplitude instead of the
+        # 16 complex MACs: 98 of 128 flop-slots on the shared fp64 datapath.
+        gauss = os.environ.get("QRT_GAUSS", "1") != "0"
+        ex = f["fp64_tflops_ref_equiv"] * (98.0 / 128.0 if gauss else 1.0)
+        roof.update({"executed_tflops": ex, "executed_frac": ex / FP64_TENSOR_PEAK,
+                     "executed_note": "fp64 datapath slots actually issued (Gauss form: 3 DMMA products + 1 DADD "
+                                      "per amplitude = 98/128 of the reference flops)" if gauss else "real form"})
     else:
         # light passes and EVC passes: one HBM round trip (gates) / read (EVC) per pass
         roof = {"bound": "hbm", "achieved": f["hbm_gbs"], "peak": hbm_peak, "unit": "GB/s", "frac": f["hbm_frac"],

@@ -1197,6 +1197,26 @@ void pauli_plan_info(int nl, int n_terms, const std::uint64_t* x, const std::uin
     int coset_groups = 0;
     for (const auto& cp : plan.cosets)
         for (int si = 0; si < cp->n_sets; ++si) coset_groups += cp->sets[si].g_count;
+    if (std::getenv("QRT_DEBUG_PLAN")) {
+        int fast = 0, distinct = 0, sets = 0, hist[8] = {};
+        for (const auto& cp : plan.cosets)
+            for (int si = 0; si < cp->n_sets; ++si) {
+                const CosetSet& S = cp->sets[si];
+                ++sets;
+                for (int xq = 1; xq < 32; ++xq) {
+                    const int n = S.xbeg[xq] - S.xbeg[xq - 1];
+                    if (n > 0) {
+                        fast += n;
+                        ++distinct;
+                        ++hist[n < 7 ? n : 7];
+                    }
+                }
+            }
+        std::fprintf(stderr, "evc cosets: %d sets, %d fast groups over %d (set, mask) pairs; per-pair counts 1..7+:",
+                     sets, fast, distinct);
+        for (int i = 1; i < 8; ++i) std::fprintf(stderr, " %d", hist[i]);
+        std::fprintf(stderr, "\n");
+    }
     if (groups) *groups = static_cast<int>(plan.dgroups.size()) + coset_groups;
     if (wide_groups) *wide_groups = static_cast<int>(plan.wgroups.size());
     if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();

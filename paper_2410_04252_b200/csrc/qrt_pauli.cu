@@ -1212,8 +1212,14 @@ void pauli_plan_info(int nl, int n_terms, const std::uint64_t* x, const std::uin
                     }
                 }
             }
-        std::fprintf(stderr, "evc cosets: %d sets, %d fast groups over %d (set, mask) pairs; per-pair counts 1..7+:",
-                     sets, fast, distinct);
+        int dpasses = 0, dwords = 0;
+        for (const auto& cp : plan.cosets)
+            if (cp->d_count > 0) {
+                ++dpasses;
+                dwords += cp->d_count;
+            }
+        std::fprintf(stderr, "evc cosets: %d I/Z words in %d passes; %d sets, %d fast groups over %d (set, mask) pairs; "
+                     "per-pair counts 1..7+:", dwords, dpasses, sets, fast, distinct);
         for (int i = 1; i < 8; ++i) std::fprintf(stderr, " %d", hist[i]);
         std::fprintf(stderr, "\n");
     }

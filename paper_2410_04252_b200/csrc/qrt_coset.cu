@@ -49,6 +49,60 @@ __device__ __forceinline__ double coset_group(const double2 (&a)[32], const doub
     return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
+// Single-bit register mask XQ (linear passes), any table mode: the 16 pairs
+// (r, r^XQ) from registers; mode 0 tables weight Re(w) only, mode 1 tables
+// (64 doubles) map (Re w, Im w) to the complex accumulator.
+template <int XQ>
+__device__ __forceinline__ double2 coset_one(const double2 (&a)[32], const double* __restrict__ T, int mode) {
+    constexpr int H = top_bit(XQ);
+    const double2* __restrict__ T2 = reinterpret_cast<const double2*>(T);  // tables are 16-byte aligned
+    double2 acc = make_double2(0.0, 0.0);
+    if (mode != 1) {  // one real table over Re(w) (mode 0) or Im(w) (mode 2)
+        const bool im = mode == 2;
+        double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+            const double2 t = T2[h];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int rho = 2 * h + u, r = ins0(rho, H), s = r ^ XQ;
+                const double2 A = a[s], B = a[r];
+                const double w = im ? fma(A.x, B.y, -A.y * B.x) : fma(A.x, B.x, A.y * B.y);
+                s4[rho & 3] = fma(u ? t.y : t.x, w, s4[rho & 3]);
+            }
+        }
+        acc.x = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    } else {
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+            const double2 t0 = T2[h], t1 = T2[8 + h], t2 = T2[16 + h], t3 = T2[24 + h];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int rho = 2 * h + u, r = ins0(rho, H), s = r ^ XQ;
+                const double2 A = a[s], B = a[r];
+                const double re = fma(A.x, B.x, A.y * B.y), im = fma(A.x, B.y, -A.y * B.x);
+                acc.x = fma(u ? t0.y : t0.x, re, fma(u ? t2.y : t2.x, im, acc.x));
+                acc.y = fma(u ? t1.y : t1.x, re, fma(u ? t3.y : t3.x, im, acc.y));
+            }
+        }
+    }
+    return acc;
+}
+
+template <int K>
+__device__ __forceinline__ void coset_ones(const double2 (&a)[32], const CosetParams& P, const CosetSet& S,
+                                           const double* __restrict__ tabs, int& g, std::uint64_t W, std::uint64_t pe,
+                                           double2& acc) {
+    const int n = S.one_cnt[K];
+    for (int i = 0; i < n; ++i, ++g) {
+        const CosetGroup& G = P.groups[g];
+        const double2 r = coset_one<1 << K>(a, tabs + G.tab, G.mode);
+        const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
+        acc.x += odd ? -r.x : r.x;
+        acc.y += odd ? -r.y : r.y;
+    }
+}
+
 // Any flip mask / table mode, pairs read from the shared-memory tile
 // (groups outside the Jordan-Wigner fast set: odd weights, Im(w) terms,
 // complex coefficients).
@@ -114,7 +168,7 @@ __device__ __forceinline__ double2 block_sum(double2 v, double2* scratch) {
     return r;
 }
 
-template <int MINB, bool GENERIC>
+template <int MINB, bool GENERIC, bool ONES>
 __global__ void __launch_bounds__(kCosetThreads, MINB)
     coset_pass_kernel(const __grid_constant__ CosetParams P, const CosetDiagTerm* __restrict__ dterms,
                       double* __restrict__ red) {
@@ -131,12 +185,14 @@ __global__ void __launch_bounds__(kCosetThreads, MINB)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(P.gtabs + 2 * i));
     }
 
-    const u64 b = static_cast<u64>(blockIdx.x);  // bit i <-> outer_pos[i]
+    const u64 b = static_cast<u64>(blockIdx.x);  // bit i <-> outer axis i
     u64 base = 0;
-    for (int i = 0; i < P.n_outer; ++i) base |= ((b >> i) & 1ull) << P.outer_pos[i];
+    for (int i = 0; i < P.n_outer; ++i)
+        if ((b >> i) & 1ull) base ^= P.outer_vec[i];
     for (int h = t; h < (1 << (kTileBits - c)); h += kCosetThreads) {
         u64 o = 0;
-        for (int i = c; i < kTileBits; ++i) o |= static_cast<u64>((h >> (i - c)) & 1) << P.tile_pos[i];
+        for (int i = c; i < kTileBits; ++i)
+            if ((h >> (i - c)) & 1) o ^= P.tile_vec[i];
         tabo[h] = o;
     }
     __syncthreads();
@@ -145,7 +201,7 @@ __global__ void __launch_bounds__(kCosetThreads, MINB)
     const int cmask = (1 << c) - 1;
     for (int e = t; e < E; e += kCosetThreads) {
         const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&tile[swz(e)]));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(&v[base | tabo[e >> c] | (e & cmask)]));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(&v[base ^ tabo[e >> c] ^ (e & cmask)]));
     }
     asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
@@ -213,8 +269,17 @@ __global__ void __launch_bounds__(kCosetThreads, MINB)
         coset_fast<27>(a, P, S, stab, present, W, pe, acc);
         coset_fast<29>(a, P, S, stab, present, W, pe, acc);
         coset_fast<30>(a, P, S, stab, present, W, pe, acc);
+        int g1 = S.g_begin + S.xbeg[31];
+        if (ONES) {
+            const double* __restrict__ dt = reinterpret_cast<const double*>(stab);
+            coset_ones<0>(a, P, S, dt, g1, W, pe, acc);
+            coset_ones<1>(a, P, S, dt, g1, W, pe, acc);
+            coset_ones<2>(a, P, S, dt, g1, W, pe, acc);
+            coset_ones<3>(a, P, S, dt, g1, W, pe, acc);
+            coset_ones<4>(a, P, S, dt, g1, W, pe, acc);
+        }
         if (GENERIC)
-        for (int g = S.g_begin + S.xbeg[31]; g < S.g_begin + S.g_count; ++g) {
+        for (int g = g1; g < S.g_begin + S.g_count; ++g) {
             const CosetGroup& G = P.groups[g];
             const double2 r = coset_generic(tile, sb, swq, G.xq, G.mode, P.tabs + G.tab);
             const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
@@ -242,13 +307,19 @@ void launch_coset_pass(const CosetParams& P, const CosetDiagTerm* dterms, int pe
         const char* e = std::getenv("QRT_COSET_OCC");
         return (e && std::atoi(e) == 3) ? 3 : 2;
     }();
-    bool generic = false;
-    for (int i = 0; i < P.n_sets; ++i) generic = generic || P.sets[i].xbeg[31] < P.sets[i].g_count;
+    bool generic = false, any_ones = false;
+    for (int i = 0; i < P.n_sets; ++i) {
+        int ones = 0;
+        for (int k = 0; k < kCosetBits; ++k) ones += P.sets[i].one_cnt[k];
+        generic = generic || P.sets[i].xbeg[31] + ones < P.sets[i].g_count;
+        any_ones = any_ones || ones > 0;
+    }
     static bool attr_done[64] = {};
     if (!attr_done[device]) {
-        QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
-        QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
-        QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
+        QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<2, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
+        QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
+        QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<2, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
+        QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<3, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
         attr_done[device] = true;
     }
     const std::size_t smem = (std::size_t{1} << kTileBits) * sizeof(double2) +
@@ -256,12 +327,16 @@ void launch_coset_pass(const CosetParams& P, const CosetDiagTerm* dterms, int pe
                              static_cast<std::size_t>(P.n_tab) * sizeof(double) +
                              (P.d_count > 0 ? (std::size_t{1} << kTileBits) * sizeof(double) : 0);
     dim3 grid(static_cast<unsigned>(P.tiles_per_pe), static_cast<unsigned>(pe_count));
+    // single-bit-mask groups (linear passes) get their own instantiations so
+    // the Jordan-Wigner fast kernel keeps its register allocation
     if (generic)
-        coset_pass_kernel<2, true><<<grid, kCosetThreads, smem, stream>>>(P, dterms, red);
+        coset_pass_kernel<2, true, true><<<grid, kCosetThreads, smem, stream>>>(P, dterms, red);
+    else if (any_ones)
+        coset_pass_kernel<2, false, true><<<grid, kCosetThreads, smem, stream>>>(P, dterms, red);
     else if (occ == 2)
-        coset_pass_kernel<2, false><<<grid, kCosetThreads, smem, stream>>>(P, dterms, red);
+        coset_pass_kernel<2, false, false><<<grid, kCosetThreads, smem, stream>>>(P, dterms, red);
     else
-        coset_pass_kernel<3, false><<<grid, kCosetThreads, smem, stream>>>(P, dterms, red);
+        coset_pass_kernel<3, false, false><<<grid, kCosetThreads, smem, stream>>>(P, dterms, red);
     QRT_CUDA(cudaGetLastError());
 }
 

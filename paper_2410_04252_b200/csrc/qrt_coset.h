@@ -34,7 +34,8 @@ struct CosetGroup {
     std::uint64_t gz;  // sign bits over the PE index
     std::int16_t tab;  // first double of the group's table(s) in CosetParams::tabs
     std::int8_t xq;    // flip mask over the coset's register bits (nonzero)
-    std::int8_t mode;  // 0: Re(w) only with real coefficients (16 doubles), 1: general (64 doubles)
+    std::int8_t mode;  // 0: Re(w) only with real coefficients (16 doubles), 1: general (64 doubles),
+                       // 2: Im(w) only with real coefficients (16 doubles; single-bit masks only)
 };
 
 struct CosetSet {
@@ -42,10 +43,11 @@ struct CosetSet {
     std::int8_t tb[kTileBits - kCosetBits];   // tile bit of thread-index bit i
     std::int16_t g_begin, g_count;
     std::uint32_t present;  // bit x: some fast group has mask x
-    std::uint8_t xbeg[32];  // fast groups sorted by mask: [xbeg[x-1], xbeg[x]) have mask x; generic from xbeg[31]
+    std::uint8_t xbeg[32];  // fast groups sorted by mask: [xbeg[x-1], xbeg[x]) have mask x
+    std::uint8_t one_cnt[kCosetBits];  // then single-bit-mask groups: one_cnt[k] with mask 1 << k; generic after them
 };
 
-// W = tile index (bits 0..11) | outer index of the CTA (bit 12 + i <-> outer_pos[i]).
+// W = tile index (bits 0..11) | outer index of the CTA (bit 12 + i <-> outer axis i).
 struct CosetParams {
     const amp_t* ptrs[kMaxLocalPEs];
     int c;
@@ -56,8 +58,13 @@ struct CosetParams {
     int d_begin, d_count;  // I/Z words of this pass (global term array), Walsh-Hadamard path
     int n_tab;             // doubles of tabs in use (staged in shared memory)
     const double* gtabs;   // device copy of tabs[0, n_tab) (coalesced staging)
-    std::int8_t tile_pos[kTileBits];
-    std::int8_t outer_pos[64];
+    // Tile / outer axes as index vectors: element (outer b, tile e) sits at
+    //   XOR_i b_i outer_vec[i]  ^  XOR_{i >= c} e_i tile_vec[i]  ^  (e & (2^c - 1)).
+    // Ordinary passes use unit vectors (axes = positions); *linear* passes
+    // (wide flip masks) use a GF(2) basis whose tile axes are the flip masks
+    // themselves, so every batched group flips a single tile bit.
+    std::uint64_t tile_vec[kTileBits];
+    std::uint64_t outer_vec[64];
     CosetSet sets[kCosetMaxSets];
     CosetGroup groups[kCosetMaxGroups];
     double tabs[kCosetMaxTab];

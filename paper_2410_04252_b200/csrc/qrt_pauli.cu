@@ -455,6 +455,7 @@ struct PauliPlanHost {
     std::vector<std::unique_ptr<CosetParams>> cosets;  // register-coset passes
     std::vector<CosetDiagTerm> cdterms;
     int coset_sets = 0;
+    int linear_passes = 0;  // coset launches on GF(2)-linear tiles (wide flip masks)
 };
 
 namespace {
@@ -469,10 +470,14 @@ bool coset_enabled() {
 // Groups are covered greedily by 5-bit register sets Q; within a set each
 // group is split by the sign bits its terms have outside Q (so that one
 // thread sign serves all of them) and folded into a 16-entry table.
+// sm[t]: the sign mask (Z|Y) of term t in the pass's coordinates; y only
+// supplies Y counts.  cols (nullptr: unit vectors) maps each coordinate axis
+// p to its index vector (linear passes, see CosetParams::tile_vec).
 void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B,
                       const std::vector<std::pair<std::uint64_t, std::vector<int>>>& flips, const std::vector<int>& gidx,
-                      const std::vector<int>& diag, const std::uint64_t* y, const std::uint64_t* z,
-                      const std::uint64_t* gz, const double* coeffs, const std::vector<std::uint64_t>* qsets) {
+                      const std::vector<int>& diag, const std::uint64_t* y, const std::uint64_t* sm,
+                      const std::uint64_t* gz, const double* coeffs, const std::vector<std::uint64_t>* qsets,
+                      const std::uint64_t* cols = nullptr) {
     int tile_pos[kTileBits], outer_pos[64], tb_of[64], ob_of[64];
     int ti = 0, no = 0;
     for (int p = 0; p < 64; ++p) tb_of[p] = ob_of[p] = -1;
@@ -485,8 +490,8 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
             outer_pos[no++] = p;
         }
     }
-    int c = 0;
-    while (c < kTileBits && tile_pos[c] == c) ++c;
+    int c = 0;  // leading tile axes that are the unit positions 0..c-1 (addressed directly)
+    while (c < kTileBits && tile_pos[c] == c && (!cols || cols[c] == (1ull << c))) ++c;
     auto to_tile = [&](std::uint64_t m) {
         int r = 0;
         for (int i = 0; i < kTileBits; ++i) r |= static_cast<int>((m >> tile_pos[i]) & 1ull) << i;
@@ -499,8 +504,8 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
         P->n_outer = no;
         P->pe_begin = pe_begin;
         P->tiles_per_pe = 1 << (nl - kTileBits);
-        for (int i = 0; i < kTileBits; ++i) P->tile_pos[i] = static_cast<std::int8_t>(tile_pos[i]);
-        for (int i = 0; i < no; ++i) P->outer_pos[i] = static_cast<std::int8_t>(outer_pos[i]);
+        for (int i = 0; i < kTileBits; ++i) P->tile_vec[i] = cols ? cols[tile_pos[i]] : 1ull << tile_pos[i];
+        for (int i = 0; i < no; ++i) P->outer_vec[i] = cols ? cols[outer_pos[i]] : 1ull << outer_pos[i];
         return P;
     };
     auto P = fresh();
@@ -510,7 +515,7 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
         P->d_count = static_cast<int>(diag.size());
         for (int t : diag) {
             CosetDiagTerm tm{};
-            tm.m = z[t] | y[t];
+            tm.m = sm[t];
             tm.gz = gz[t];
             tm.f = make_double2(coeffs[2 * t], coeffs[2 * t + 1]);
             tm.m_tile = to_tile(tm.m & B);
@@ -621,7 +626,7 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
         for (int g : in) {
             const int xq = to_reg(xt[static_cast<std::size_t>(g)]);
             for (int t : flips[static_cast<std::size_t>(g)].second) {
-                const std::uint64_t m = z[t] | y[t];
+                const std::uint64_t m = sm[t];
                 const std::uint64_t mf = to_w(m);
                 auto it = std::find_if(subs.begin(), subs.end(), [&](const Sub& u) {
                     return u.xq == xq && u.mf == mf && u.gz == gz[t];
@@ -642,10 +647,14 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
                 if ((__builtin_popcountll(y[t]) & 1) || coeffs[2 * t + 1] != 0.0) return false;
             return true;
         };
+        // then the single-bit masks (linear passes; any table mode, evaluated
+        // from the register coset), sorted by mask; the generic ones last
+        auto one_of = [&](const Sub& u) { return !fast_of(u) && __builtin_popcount(static_cast<unsigned>(u.xq)) == 1; };
+        auto cls = [&](const Sub& u) { return fast_of(u) ? 0 : one_of(u) ? 1 : 2; };
         std::stable_sort(subs.begin(), subs.end(), [&](const Sub& a, const Sub& b) {
-            const bool fa = fast_of(a), fb = fast_of(b);
-            if (fa != fb) return fa;
-            return fa && a.xq < b.xq;
+            const int ca = cls(a), cb = cls(b);
+            if (ca != cb) return ca < cb;
+            return ca < 2 && a.xq < b.xq;
         });
         // emit in chunks that fit the launch parameters (a set whose
         // subgroups overflow one launch is repeated with the same Q)
@@ -654,13 +663,19 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
                 if ((__builtin_popcountll(y[t]) & 1) || coeffs[2 * t + 1] != 0.0) return false;
             return true;
         };
+        auto im_real_of = [&](const Sub& u) {  // Im(w) only (odd Y counts), real coefficients
+            for (int t : u.terms)
+                if (!(__builtin_popcountll(y[t]) & 1) || coeffs[2 * t + 1] != 0.0) return false;
+            return true;
+        };
         std::size_t at = 0;
         while (at < subs.size()) {
             auto room = [&](std::size_t from) {
                 std::size_t end = from;
                 int g = n_groups, tb = n_tab;
                 while (end < subs.size() && end - from < 255) {
-                    const int need = re_real_of(subs[end]) ? 16 : 64;
+                    const int need =
+                        (re_real_of(subs[end]) || (one_of(subs[end]) && im_real_of(subs[end]))) ? 16 : 64;
                     if (g + 1 > kCosetMaxGroups || tb + need > kCosetMaxTab) break;
                     ++g;
                     tb += need;
@@ -687,6 +702,11 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
             Sc.present = 0;
             for (std::size_t q = at; q < end; ++q)
                 if (fast_of(subs[q])) Sc.present |= 1u << subs[q].xq;
+            for (int k = 0; k < kCosetBits; ++k) {
+                int cnt = 0;
+                for (std::size_t q = at; q < end; ++q) cnt += one_of(subs[q]) && subs[q].xq == (1 << k);
+                Sc.one_cnt[k] = static_cast<std::uint8_t>(cnt);  // single-bit subgroups, after the fast ones
+            }
             for (std::size_t q = at; q < end; ++q) {
                 const Sub& u = subs[q];
                 CosetGroup& G = P->groups[n_groups++];
@@ -695,20 +715,22 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
                 G.gz = u.gz;
                 G.tab = static_cast<std::int16_t>(n_tab);
                 const bool re_real = re_real_of(u);
-                G.mode = re_real ? 0 : 1;
+                const bool im_real = !re_real && one_of(u) && im_real_of(u);
+                G.mode = re_real ? 0 : im_real ? 2 : 1;
                 const int H = 31 - __builtin_clz(static_cast<unsigned>(u.xq));
                 double* T = P->tabs + n_tab;
-                n_tab += re_real ? 16 : 64;
-                for (int e = 0; e < (re_real ? 16 : 64); ++e) T[e] = 0.0;
+                const int tl = G.mode == 1 ? 64 : 16;
+                n_tab += tl;
+                for (int e = 0; e < tl; ++e) T[e] = 0.0;
                 for (int t : u.terms) {
                     const int ycnt = __builtin_popcountll(y[t]);
                     const double sgn = ((ycnt & 3) == 1 || (ycnt & 3) == 2) ? -2.0 : 2.0;
                     const double fx = sgn * coeffs[2 * t], fy = sgn * coeffs[2 * t + 1];
-                    const int mq = to_reg(to_tile((z[t] | y[t]) & B));
+                    const int mq = to_reg(to_tile((sm[t]) & B));
                     for (int rho = 0; rho < 16; ++rho) {
                         const int r = ((rho >> H) << (H + 1)) | (rho & ((1 << H) - 1));
                         const double sg = (__builtin_popcount(static_cast<unsigned>(r & mq)) & 1) ? -1.0 : 1.0;
-                        if (re_real) {
+                        if (re_real || im_real) {  // mode 0 weights Re(w), mode 2 Im(w), into the real part
                             T[rho] += sg * fx;
                         } else if (ycnt & 1) {
                             T[32 + rho] += sg * fx;
@@ -800,12 +822,21 @@ PauliPlanHost build_pauli_plan(int nl, int pe_begin, int n_terms, const std::uin
     const int T = std::min(kTileBits, nl);
     const int coal = std::min(kCoalBits, nl);
     const std::uint64_t coal_mask = (1ull << coal) - 1;
+    std::vector<std::uint64_t> zy(static_cast<std::size_t>(n_terms));
+    for (int t = 0; t < n_terms; ++t) zy[static_cast<std::size_t>(t)] = z[t] | y[t];
     std::vector<int> diag;
     std::vector<std::pair<std::uint64_t, std::vector<int>>> flips, wide;
+    // wide flip masks (and, on linear passes, any mask too heavy for a
+    // register coset) go to linear passes (GF(2) tile axes = the masks)
+    // unless QRT_EVC_LINEAR=0
+    const bool linear = coset_enabled() && nl >= kTileBits && T == kTileBits && [] {
+        const char* e = std::getenv("QRT_EVC_LINEAR");
+        return e ? std::atoi(e) != 0 : true;
+    }();
     for (auto& kv : by_xy) {
         if (kv.first == 0)
             diag = kv.second;
-        else if (popc(kv.first | coal_mask) > T)
+        else if (popc(kv.first | coal_mask) > T || (linear && popc(kv.first) > kCosetBits))
             wide.emplace_back(kv.first, kv.second);
         else
             flips.emplace_back(kv.first, kv.second);
@@ -819,7 +850,8 @@ PauliPlanHost build_pauli_plan(int nl, int pe_begin, int n_terms, const std::uin
         std::vector<std::uint64_t> qsets;  // register sets of the global cover (coset passes)
     };
     std::vector<Pass> passes;
-    bool global_cover = coset_enabled() && nl >= kTileBits && T == kTileBits && !flips.empty() && wide.empty();
+    bool global_cover = coset_enabled() && nl >= kTileBits && T == kTileBits && !flips.empty() &&
+                        (wide.empty() || linear);
     {
         const char* e = std::getenv("QRT_EVC_GLOBAL_COVER");
         if (e && std::atoi(e) == 0) global_cover = false;
@@ -955,8 +987,8 @@ PauliPlanHost build_pauli_plan(int nl, int pe_begin, int n_terms, const std::uin
         for (int gi : ps.groups)
             if (popc(flips[static_cast<std::size_t>(gi)].first) > kCosetBits) coset = false;
         if (coset) {
-            build_coset_pass(plan, nl, pe_begin, ps.B, flips, ps.groups, ps.has_diag ? diag : std::vector<int>{}, y, z,
-                             gz, coeffs, ps.qsets.empty() ? nullptr : &ps.qsets);
+            build_coset_pass(plan, nl, pe_begin, ps.B, flips, ps.groups, ps.has_diag ? diag : std::vector<int>{}, y,
+                             zy.data(), gz, coeffs, ps.qsets.empty() ? nullptr : &ps.qsets);
             continue;
         }
         PPass h{};
@@ -1040,6 +1072,65 @@ PauliPlanHost build_pauli_plan(int nl, int pe_begin, int n_terms, const std::uin
         }
         h.g_count = static_cast<int>(dgroups.size()) - h.g_begin;
         hdrs.push_back(h);
+    }
+    // wide flip masks, linear passes: batches of up to T - coal groups whose
+    // masks are independent above the coalescing bits.  In the pass's
+    // coordinates i' (i = A^-1 i', column p of A^-1 = cols[p]) the k-th mask
+    // is the unit vector of its pivot position piv_k (cols[piv_k] = the mask),
+    // the other axes stay unit vectors, and a sign mask m becomes
+    // m'_p = parity(cols[p] & m).  One HBM read of the state then serves the
+    // whole batch instead of one read per group.
+    if (linear && !wide.empty()) {
+        std::vector<std::size_t> pending(wide.size());
+        for (std::size_t i = 0; i < wide.size(); ++i) pending[i] = i;
+        const std::uint64_t coal_m = (1ull << coal) - 1;
+        std::vector<std::uint64_t> smL(static_cast<std::size_t>(n_terms), 0);
+        while (!pending.empty()) {
+            std::vector<std::uint64_t> basis;
+            std::vector<int> piv;
+            std::vector<std::size_t> batch, rest;
+            for (std::size_t w : pending) {
+                if (static_cast<int>(batch.size()) == T - coal) {
+                    rest.push_back(w);
+                    continue;
+                }
+                std::uint64_t v = wide[w].first & ~coal_m;
+                for (std::size_t k = 0; k < basis.size(); ++k)
+                    if (v >> piv[k] & 1ull) v ^= basis[k];
+                if (!v) {
+                    rest.push_back(w);
+                    continue;
+                }
+                basis.push_back(v);
+                piv.push_back(63 - __builtin_clzll(v));
+                batch.push_back(w);
+            }
+            std::uint64_t cols[64];
+            for (int p = 0; p < 64; ++p) cols[p] = 1ull << p;
+            std::uint64_t B = coal_m;
+            for (std::size_t k = 0; k < batch.size(); ++k) {
+                cols[piv[k]] = wide[batch[k]].first;
+                B |= 1ull << piv[k];
+            }
+            for (int p = coal; p < nl && popc(B) < T; ++p) B |= 1ull << p;
+            std::vector<std::pair<std::uint64_t, std::vector<int>>> fl;
+            std::vector<int> gi;
+            for (std::size_t k = 0; k < batch.size(); ++k) {
+                fl.emplace_back(1ull << piv[k], wide[batch[k]].second);
+                gi.push_back(static_cast<int>(k));
+                for (int t : wide[batch[k]].second) {
+                    std::uint64_t m = 0;
+                    for (int p = 0; p < nl; ++p)
+                        m |= static_cast<std::uint64_t>(popc(cols[p] & zy[static_cast<std::size_t>(t)]) & 1) << p;
+                    smL[static_cast<std::size_t>(t)] = m;
+                }
+            }
+            build_coset_pass(plan, nl, pe_begin, B, fl, gi, std::vector<int>{}, y, smL.data(), gz, coeffs, nullptr,
+                             cols);
+            ++plan.linear_passes;
+            pending.swap(rest);
+        }
+        wide.clear();
     }
     // wide flip masks: full-vector sweeps (terms keep their full sign masks)
     for (const auto& [xy, members] : wide) {
@@ -1191,8 +1282,8 @@ void pauli_plan_info(int nl, int n_terms, const std::uint64_t* x, const std::uin
     PauliPlanHost plan = build_pauli_plan(nl, 0, n_terms, x, y, z, gz, coeffs);
     const auto t1 = std::chrono::steady_clock::now();
     if (std::getenv("QRT_DEBUG_PLAN"))
-        std::fprintf(stderr, "evc plan: %zu tiled passes, %zu coset launches, %d coset sets, %zu wide groups\n",
-                     plan.hdrs.size(), plan.cosets.size(), plan.coset_sets, plan.wgroups.size());
+        std::fprintf(stderr, "evc plan: %zu tiled passes, %zu coset launches (%d linear), %d coset sets, %zu wide groups\n",
+                     plan.hdrs.size(), plan.cosets.size(), plan.linear_passes, plan.coset_sets, plan.wgroups.size());
     if (passes) *passes = static_cast<int>(plan.hdrs.size() + plan.cosets.size());
     int coset_groups = 0;
     for (const auto& cp : plan.cosets)

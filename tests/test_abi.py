@@ -104,5 +104,20 @@ def test_evc_pass_plan_host_only(qb):
 
     rng = np.random.default_rng(1)
     rnd = [qb.PauliTerm(1.0, "".join("IXYZ"[int(v)] for v in rng.integers(0, 4, 30))) for _ in range(50)]
-    _, _, wide_r, _ = _plan_info(qb, rnd)
-    assert wide_r > 0  # random words need the full-vector path
+    passes_r, groups_r, wide_r, _ = _plan_info(qb, rnd)
+    # random words: flip masks wider than a tile go to GF(2)-linear passes,
+    # up to 8 groups per HBM read of the state, none to full-vector sweeps
+    assert wide_r == 0 and groups_r == 50 and passes_r <= 8
+
+
+def test_evc_linear_passes_knob(qb, monkeypatch):
+    """QRT_EVC_LINEAR=0 restores one full-vector sweep per wide group."""
+    import numpy as np
+
+    rng = np.random.default_rng(3)
+    rnd = [qb.PauliTerm(1.0, "".join("IXYZ"[int(v)] for v in rng.integers(0, 4, 28))) for _ in range(40)]
+    monkeypatch.setenv("QRT_EVC_LINEAR", "0")
+    _, _, wide_off, _ = _plan_info(qb, rnd)
+    monkeypatch.setenv("QRT_EVC_LINEAR", "1")
+    passes_on, _, wide_on, _ = _plan_info(qb, rnd)
+    assert wide_off > 30 and wide_on == 0 and passes_on <= 6

@@ -304,15 +304,20 @@ def test_large_qr_roundtrip_and_norm(qb, device):
     assert abs(st.norm() - 1.0) <= 1e-12
 
 
-@pytest.mark.parametrize("n,p", [(16, 1), (16, 2), (18, 4)])
-def test_expectation_uniform_random_strings(qb, device, n, p):
+@pytest.mark.parametrize("n,p,k,linear", [(16, 1, 60, 1), (16, 2, 60, 1), (18, 4, 60, 1), (20, 1, 150, 1),
+                                          (20, 2, 150, 1), (18, 2, 60, 0)])
+def test_expectation_uniform_random_strings(qb, device, monkeypatch, n, p, k, linear):
     """Uniformly random words (SURVEY §8d C5 stress): most flip masks are wider
-    than a shared-memory tile and take the full-vector path."""
-    rng = np.random.default_rng(2024 + n + p)
+    than a shared-memory tile and take the GF(2)-linear passes (8 groups per
+    HBM read); QRT_EVC_LINEAR=0 the full-vector sweeps (one per group)."""
+    monkeypatch.setenv("QRT_EVC_LINEAR", str(linear))
+    rng = np.random.default_rng(2024 + n + p + 100 * (1 - linear))  # distinct words: no plan-cache hit
     terms = []
-    for _ in range(60):
+    for _ in range(k):
         letters = "".join("IXYZ"[int(rng.integers(4))] for _ in range(n))
-        terms.append(qb.PauliTerm(complex(rng.uniform(-1, 1), rng.uniform(-0.1, 0.1)), letters))
+        # the 150-word cases use real coefficients (single-table Re(w) / Im(w) groups)
+        im = 0.0 if k == 150 else rng.uniform(-0.1, 0.1)
+        terms.append(qb.PauliTerm(complex(rng.uniform(-1, 1), im), letters))
     psi = qb.random_state(n, 77 + n)
     shape = qb.ClusterShape.flat(p)
     plan = qb.plan_evc(terms, n, shape, True, 4)

@@ -1204,7 +1204,7 @@ GatePlan plan_gates(int nl, int n_gates, const int* arity, const int* pos, const
     if (!cached && env_on("QRT_PLAN_CACHE", true)) {
         std::lock_guard<std::mutex> lock(plan_mu);
         plan_cache.emplace_back(std::move(skey), std::make_shared<const std::vector<GatePass>>(passes));
-        if (plan_cache.size() > 16) plan_cache.pop_front();
+        if (plan_cache.size() > 512) plan_cache.pop_front();
     }
 
     lap("plan");

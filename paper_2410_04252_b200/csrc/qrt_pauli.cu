@@ -1190,7 +1190,8 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
     if (!plan_ptr) {
         plan_ptr = std::make_shared<PauliPlanHost>(build_pauli_plan(nl, st->pe_begin, n_terms, x, y, z, gz, coeffs));
         cache.emplace_back(std::move(key), plan_ptr);
-        if (cache.size() > 8) cache.pop_front();
+        // one entry per EVC plan tile of the Hamiltonian (uniform 10k words: 26-60 tiles)
+        if (cache.size() > 96) cache.pop_front();
     }
     PauliPlanHost& plan = *plan_ptr;
     const int T = plan.T;

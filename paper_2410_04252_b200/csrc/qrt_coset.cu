@@ -5,6 +5,7 @@
 // evaluated pair-wise over the canonical half of each flip-mask group.
 // One CTA = one 2^12-amplitude tile = 128 threads x 32-amplitude cosets.
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "qrt_coset.h"
@@ -168,6 +169,70 @@ __device__ __forceinline__ double2 block_sum(double2 v, double2* scratch) {
     return r;
 }
 
+// Every coset set of the pass over one tile (128 threads; t = thread index
+// within them): load the thread's 32-amplitude coset into registers, then
+// the fast (weight-2/4), single-bit and generic groups of the set.
+template <bool GENERIC, bool ONES>
+__device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const double2* __restrict__ tile,
+                                                const double2* __restrict__ stab, int t, u64 wout, u64 pe,
+                                                double2& acc) {
+    for (int s = 0; s < P.n_sets; ++s) {
+        const CosetSet& S = P.sets[s];
+        int ebase = 0;
+#pragma unroll
+        for (int i = 0; i < kTileBits - kCosetBits; ++i) ebase |= ((t >> i) & 1) << S.tb[i];
+        int swq[kCosetBits];
+#pragma unroll
+        for (int q = 0; q < kCosetBits; ++q) swq[q] = swz(1 << S.S[q]);
+        const int sb = swz(ebase);
+        double2 a[32];
+        {
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+                int o = sb;
+#pragma unroll
+                for (int q = 0; q < kCosetBits; ++q)
+                    if ((r >> q) & 1) o ^= swq[q];
+                a[r] = tile[o];
+            }
+        }
+        const u64 W = static_cast<u64>(ebase) | wout;
+        const unsigned present = S.present;
+        coset_fast<3>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<5>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<6>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<9>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<10>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<12>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<15>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<17>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<18>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<20>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<23>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<24>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<27>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<29>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<30>(a, P, S, stab, present, W, pe, acc);
+        int g1 = S.g_begin + S.xbeg[31];
+        if (ONES) {
+            const double* __restrict__ dt = reinterpret_cast<const double*>(stab);
+            coset_ones<0>(a, P, S, dt, g1, W, pe, acc);
+            coset_ones<1>(a, P, S, dt, g1, W, pe, acc);
+            coset_ones<2>(a, P, S, dt, g1, W, pe, acc);
+            coset_ones<3>(a, P, S, dt, g1, W, pe, acc);
+            coset_ones<4>(a, P, S, dt, g1, W, pe, acc);
+        }
+        if (GENERIC)
+        for (int g = g1; g < S.g_begin + S.g_count; ++g) {
+            const CosetGroup& G = P.groups[g];
+            const double2 r = coset_generic(tile, sb, swq, G.xq, G.mode, P.tabs + G.tab);
+            const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
+            acc.x += odd ? -r.x : r.x;
+            acc.y += odd ? -r.y : r.y;
+        }
+    }
+}
+
 template <int MINB, bool GENERIC, bool ONES>
 __global__ void __launch_bounds__(kCosetThreads, MINB)
     coset_pass_kernel(const __grid_constant__ CosetParams P, const CosetDiagTerm* __restrict__ dterms,
@@ -231,64 +296,101 @@ __global__ void __launch_bounds__(kCosetThreads, MINB)
         }
     }
 
-    const u64 wout = b << kTileBits;
-    for (int s = 0; s < P.n_sets; ++s) {
-        const CosetSet& S = P.sets[s];
-        int ebase = 0;
-#pragma unroll
-        for (int i = 0; i < kTileBits - kCosetBits; ++i) ebase |= ((t >> i) & 1) << S.tb[i];
-        int swq[kCosetBits];
-#pragma unroll
-        for (int q = 0; q < kCosetBits; ++q) swq[q] = swz(1 << S.S[q]);
-        const int sb = swz(ebase);
-        double2 a[32];
-        {
-#pragma unroll
-            for (int r = 0; r < 32; ++r) {
-                int o = sb;
-#pragma unroll
-                for (int q = 0; q < kCosetBits; ++q)
-                    if ((r >> q) & 1) o ^= swq[q];
-                a[r] = tile[o];
-            }
-        }
-        const u64 W = static_cast<u64>(ebase) | wout;
-        const unsigned present = S.present;
-        coset_fast<3>(a, P, S, stab, present, W, pe, acc);
-        coset_fast<5>(a, P, S, stab, present, W, pe, acc);
-        coset_fast<6>(a, P, S, stab, present, W, pe, acc);
-        coset_fast<9>(a, P, S, stab, present, W, pe, acc);
-        coset_fast<10>(a, P, S, stab, present, W, pe, acc);
-        coset_fast<12>(a, P, S, stab, present, W, pe, acc);
-        coset_fast<15>(a, P, S, stab, present, W, pe, acc);
-        coset_fast<17>(a, P, S, stab, present, W, pe, acc);
-        coset_fast<18>(a, P, S, stab, present, W, pe, acc);
-        coset_fast<20>(a, P, S, stab, present, W, pe, acc);
-        coset_fast<23>(a, P, S, stab, present, W, pe, acc);
-        coset_fast<24>(a, P, S, stab, present, W, pe, acc);
-        coset_fast<27>(a, P, S, stab, present, W, pe, acc);
-        coset_fast<29>(a, P, S, stab, present, W, pe, acc);
-        coset_fast<30>(a, P, S, stab, present, W, pe, acc);
-        int g1 = S.g_begin + S.xbeg[31];
-        if (ONES) {
-            const double* __restrict__ dt = reinterpret_cast<const double*>(stab);
-            coset_ones<0>(a, P, S, dt, g1, W, pe, acc);
-            coset_ones<1>(a, P, S, dt, g1, W, pe, acc);
-            coset_ones<2>(a, P, S, dt, g1, W, pe, acc);
-            coset_ones<3>(a, P, S, dt, g1, W, pe, acc);
-            coset_ones<4>(a, P, S, dt, g1, W, pe, acc);
-        }
-        if (GENERIC)
-        for (int g = g1; g < S.g_begin + S.g_count; ++g) {
-            const CosetGroup& G = P.groups[g];
-            const double2 r = coset_generic(tile, sb, swq, G.xq, G.mode, P.tabs + G.tab);
-            const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
-            acc.x += odd ? -r.x : r.x;
-            acc.y += odd ? -r.y : r.y;
-        }
-    }
+    coset_tile_sets<GENERIC, ONES>(P, tile, stab, t, b << kTileBits, pe, acc);
     const double2 tot = block_sum(acc, scratch);
     if (t == 0) {
+        double* slot = red + 2 * (static_cast<std::size_t>(blockIdx.y) * gridDim.x + blockIdx.x);
+        slot[0] += tot.x;
+        slot[1] += tot.y;
+    }
+}
+
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n)); }
+
+__device__ __forceinline__ void mbar_wait(unsigned addr, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(addr),
+        "r"(parity));
+}
+
+// Persistent, software-pipelined variant for passes without I/Z words: one
+// 256-thread CTA per SM holds three tile buffers; two teams of 128 threads
+// evaluate alternate tiles (team = tile index & 1) while the third buffer
+// fills.  Tile k lives in buffer k % 3 and is loaded by the other team right
+// after that team finished tile k - 3 in the same buffer; completion travels
+// through one mbarrier per buffer (cp.async.mbarrier.arrive.noinc, 128
+// arrivals per fill), so a team never waits for HBM while the other computes.
+template <bool GENERIC, bool ONES>
+__global__ void __launch_bounds__(2 * kCosetThreads, 1)
+    coset_pipe_kernel(const __grid_constant__ CosetParams P, double* __restrict__ red) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double2 scratch[2 * kCosetThreads / 32];
+    __shared__ __align__(8) unsigned long long full[3];
+    constexpr int E = 1 << kTileBits;
+    const int c = P.c;
+    const int team = threadIdx.x >> 7, tid = threadIdx.x & (kCosetThreads - 1);
+    double2* bufs = reinterpret_cast<double2*>(smem_raw);  // 3 x E
+    u64* tabo = reinterpret_cast<u64*>(bufs + 3 * E);
+    double2* stab = reinterpret_cast<double2*>(tabo + ((1 << (kTileBits - c)) | 1) + 1);
+    for (int i = threadIdx.x; i < (P.n_tab >> 1); i += blockDim.x) {
+        const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&stab[i]));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(P.gtabs + 2 * i));
+    }
+    for (int h = threadIdx.x; h < (1 << (kTileBits - c)); h += blockDim.x) {
+        u64 o = 0;
+        for (int i = c; i < kTileBits; ++i)
+            if ((h >> (i - c)) & 1) o ^= P.tile_vec[i];
+        tabo[h] = o;
+    }
+    if (threadIdx.x < 3) {
+        const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[threadIdx.x]));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(kCosetThreads));
+    }
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
+
+    const int tiles = P.tiles_per_pe;
+    const int stride = static_cast<int>(gridDim.x);
+    const int ntile = (tiles - static_cast<int>(blockIdx.x) + stride - 1) / stride;  // this CTA's tiles
+    const amp_t* __restrict__ v = P.ptrs[blockIdx.y];
+    const u64 pe = static_cast<u64>(P.pe_begin) + blockIdx.y;
+    const int cmask = (1 << c) - 1;
+    auto tile_of = [&](int k) { return static_cast<u64>(blockIdx.x) + static_cast<u64>(k) * stride; };
+    auto issue = [&](int k) {  // this team's 128 threads fill buffer k % 3 with tile k
+        const u64 b = tile_of(k);
+        u64 base = 0;
+        for (int i = 0; i < P.n_outer; ++i)
+            if ((b >> i) & 1ull) base ^= P.outer_vec[i];
+        double2* tile = bufs + (k % 3) * E;
+        for (int e = tid; e < E; e += kCosetThreads) {
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&tile[swz(e)]));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
+                         "l"(&v[base ^ tabo[e >> c] ^ (e & cmask)]));
+        }
+        const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[k % 3]));
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a));
+    };
+    // tile k is issued by team (k + 1) & 1
+    for (int k = 0; k < 3 && k < ntile; ++k)
+        if (((k + 1) & 1) == team) issue(k);
+
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = team; k < ntile; k += 2) {
+        const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[k % 3]));
+        mbar_wait(a, static_cast<unsigned>((k / 3) & 1));
+        coset_tile_sets<GENERIC, ONES>(P, bufs + (k % 3) * E, stab, tid, tile_of(k) << kTileBits, pe, acc);
+        named_bar(1 + team, kCosetThreads);  // the team is done reading buffer k % 3
+        if (k + 3 < ntile) issue(k + 3);
+    }
+    asm volatile("cp.async.wait_all;\n" ::);
+    const double2 tot = block_sum(acc, scratch);
+    if (threadIdx.x == 0) {
         double* slot = red + 2 * (static_cast<std::size_t>(blockIdx.y) * gridDim.x + blockIdx.x);
         slot[0] += tot.x;
         slot[1] += tot.y;
@@ -321,6 +423,33 @@ void launch_coset_pass(const CosetParams& P, const CosetDiagTerm* dterms, int pe
         QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<2, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
         QRT_CUDA(cudaFuncSetAttribute(coset_pass_kernel<3, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
         attr_done[device] = true;
+    }
+    static const bool pipe = [] {
+        const char* e = std::getenv("QRT_EVC_PIPE");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    if (pipe && P.d_count == 0 && occ == 2) {  // persistent two-team pipeline (no I/Z words)
+        static int nsm[64] = {};
+        static bool pattr[64] = {};
+        if (!nsm[device]) QRT_CUDA(cudaDeviceGetAttribute(&nsm[device], cudaDevAttrMultiProcessorCount, device));
+        if (!pattr[device]) {
+            QRT_CUDA(cudaFuncSetAttribute(coset_pipe_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+            QRT_CUDA(cudaFuncSetAttribute(coset_pipe_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+            QRT_CUDA(cudaFuncSetAttribute(coset_pipe_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+            pattr[device] = true;
+        }
+        const std::size_t psmem = 3 * (std::size_t{1} << kTileBits) * sizeof(double2) +
+                                  ((std::size_t{1} << (kTileBits - P.c)) + 2) * sizeof(std::uint64_t) +
+                                  static_cast<std::size_t>(P.n_tab) * sizeof(double);
+        dim3 pgrid(static_cast<unsigned>(std::min(nsm[device], P.tiles_per_pe)), static_cast<unsigned>(pe_count));
+        if (generic)
+            coset_pipe_kernel<true, true><<<pgrid, 2 * kCosetThreads, psmem, stream>>>(P, red);
+        else if (any_ones)
+            coset_pipe_kernel<false, true><<<pgrid, 2 * kCosetThreads, psmem, stream>>>(P, red);
+        else
+            coset_pipe_kernel<false, false><<<pgrid, 2 * kCosetThreads, psmem, stream>>>(P, red);
+        QRT_CUDA(cudaGetLastError());
+        return;
     }
     const std::size_t smem = (std::size_t{1} << kTileBits) * sizeof(double2) +
                              ((std::size_t{1} << (kTileBits - P.c)) + 2) * sizeof(std::uint64_t) +

@@ -270,7 +270,9 @@ __device__ __forceinline__ void dense_dmma(double2* __restrict__ tile, const dou
 // C fragments: output amplitudes 8 nb + 2 (lane & 3) + {0, 1}.  B fragment
 // slot ((t * NB + nb) * KB + kb) * 32 + lane holds M_t[n][k] with
 // k = 4 kb + (lane & 3), n = 8 nb + (lane >> 2), M_0 = X, M_1 = Y - X, M_2 = -(X + Y).
-template <int K>
+// HOIST: the gate's 3 D^2/32 B fragments per lane are loaded into registers
+// once (needs the 168-register budget) instead of from L1 every row-block pair.
+template <int K, bool HOIST = false>
 __device__ __forceinline__ void dense_gauss(double2* __restrict__ tile, const double* __restrict__ frag,
                                             const GateOp& op, int E) {
     constexpr int D = 1 << K, NB = D / 8, KB = D / 4;
@@ -302,6 +304,12 @@ __device__ __forceinline__ void dense_gauss(double2* __restrict__ tile, const do
         sc[nb][1] = swz(spread(8 * nb + 2 * (lane & 3) + 1));
     }
     const double* __restrict__ fl = frag + lane;
+    double bf[HOIST ? 3 * NB * KB : 1];
+    if (HOIST) {
+#pragma unroll
+        for (int f = 0; f < 3 * NB * KB; ++f) bf[f] = fl[f * 32];
+    }
+    auto B = [&](int f) { return HOIST ? bf[HOIST ? f : 0] : fl[f * 32]; };
     const int blocks = (E >> K) >> 3;
     auto row_base = [&](int rb) {
         int base = rb * 8 + (lane >> 2);
@@ -326,7 +334,7 @@ __device__ __forceinline__ void dense_gauss(double2* __restrict__ tile, const do
             const double a0 = x0[kb].x + x0[kb].y, a1 = x1[kb].x + x1[kb].y;
 #pragma unroll
             for (int nb = 0; nb < NB; ++nb) {
-                const double b = fl[(nb * KB + kb) * 32];
+                const double b = B(nb * KB + kb);
                 dmma_8x8x4(k0[nb][0], k0[nb][1], a0, b);
                 dmma_8x8x4(k1[nb][0], k1[nb][1], a1, b);
             }
@@ -336,7 +344,7 @@ __device__ __forceinline__ void dense_gauss(double2* __restrict__ tile, const do
         for (int kb = 0; kb < KB; ++kb)
 #pragma unroll
             for (int nb = 0; nb < NB; ++nb) {
-                const double bi = fl[((NB + nb) * KB + kb) * 32], br = fl[((2 * NB + nb) * KB + kb) * 32];
+                const double bi = B((NB + nb) * KB + kb), br = B((2 * NB + nb) * KB + kb);
                 if (kb == 0) {
                     dmma_8x8x4_c(re0[nb][0], re0[nb][1], x0[0].y, br, k0[nb][0], k0[nb][1]);
                     dmma_8x8x4_c(re1[nb][0], re1[nb][1], x1[0].y, br, k1[nb][0], k1[nb][1]);
@@ -487,7 +495,9 @@ __global__ void __launch_bounds__(128, MINB)
                 case 1: dense_small<1>(tile, P, pm, op, E); break;
                 case 2: dense_small<2>(tile, P, pm, op, E); break;
                 case 3:
-                    if (op.bfrag >= 0 && hdr.gauss)
+                    if (op.bfrag >= 0 && hdr.gauss == 2 && MINB == 3)
+                        dense_gauss<3, true>(tile, pf + op.bfrag, op, E);
+                    else if (op.bfrag >= 0 && hdr.gauss)
                         dense_gauss<3>(tile, pf + op.bfrag, op, E);
                     else if (op.bfrag >= 0)
                         dense_dmma<3>(tile, pf + op.bfrag, op, E);
@@ -495,7 +505,9 @@ __global__ void __launch_bounds__(128, MINB)
                         dense_small<3>(tile, P, pm, op, E);
                     break;
                 case 4:
-                    if (op.bfrag >= 0 && hdr.gauss)
+                    if (op.bfrag >= 0 && hdr.gauss == 2 && MINB == 3)
+                        dense_gauss<4, true>(tile, pf + op.bfrag, op, E);
+                    else if (op.bfrag >= 0 && hdr.gauss)
                         dense_gauss<4>(tile, pf + op.bfrag, op, E);
                     else if (op.bfrag >= 0)
                         dense_dmma<4>(tile, pf + op.bfrag, op, E);
@@ -550,12 +562,13 @@ int gate_threads() {
     return v;
 }
 
-// Register budget of the gate pass kernel: the 4-CTA launch bound (<= 128
-// registers, measured fastest); QRT_GATE_REGS=168 selects the 3-CTA bound.
+// Register budget of the gate pass kernel: the 3-CTA launch bound (<= 168
+// registers: room for the hoisted Gauss fragments, measured fastest);
+// QRT_GATE_REGS=128 selects the 4-CTA bound (fragments re-read from L1).
 int gate_minb() {
     static const int v = [] {
         const char* e = std::getenv("QRT_GATE_REGS");
-        return e && std::atoi(e) == 168 ? 3 : 4;
+        return e && std::atoi(e) == 128 ? 4 : 3;
     }();
     return v;
 }
@@ -728,7 +741,7 @@ void gauss_frags(int k, const double* m, double* dst) {
 int gauss_mode() {
     static const int v = [] {
         const char* e = std::getenv("QRT_GAUSS");
-        return e ? std::atoi(e) : 1;
+        return e ? std::atoi(e) : 2;
     }();
     return v;
 }

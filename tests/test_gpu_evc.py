@@ -85,7 +85,7 @@ def test_coset_deterministic(qb, device):
 
 
 @pytest.mark.parametrize("env", [{"QRT_EVC_GLOBAL_COVER": "0"}, {"QRT_COSET_OCC": "3"}, {"QRT_GATE_THREADS": "64"},
-                                 {"QRT_PLAN_CACHE": "0"}, {"QRT_GAUSS": "0"}, {"QRT_GATE_REGS": "168"},
+                                 {"QRT_PLAN_CACHE": "0"}, {"QRT_GAUSS": "0"}, {"QRT_GAUSS": "1"}, {"QRT_GATE_REGS": "128"},
                                  {"QRT_EVC_LINEAR": "0"}, {"QRT_EVC_PIPE": "0"}])
 def test_knobs_in_subprocess(env):
     """Knobs read once per process: a fresh process per setting, checked

@@ -14,7 +14,7 @@ $NCU --metrics gpu__time_duration.sum --csv --log-file "$OUT/launches_30q_hea.cs
     python bench.py --circuit hea --steps 1 --warmup 0 --no-cpu-baseline > "$OUT/ncu_launch_hea.log" 2>&1
 $NCU --set full --import-source on -k regex:gate_pass -s 10 -c 1 -o "$OUT/gate30" \
     python bench.py --steps 1 --warmup 0 --no-cpu-baseline > "$OUT/ncu_gate.log" 2>&1
-$NCU --set full --import-source on -k regex:coset_pass -s 10 -c 1 -o "$OUT/coset30" \
+$NCU --set full --import-source on -k regex:coset_pipe -s 10 -c 1 -o "$OUT/coset30" \
     python bench.py --steps 1 --warmup 0 --no-cpu-baseline > "$OUT/ncu_coset.log" 2>&1
 $NCU --set full --import-source on -k regex:light_pass -s 10 -c 1 -o "$OUT/light30" \
     python bench.py --circuit hea --steps 1 --warmup 0 --no-cpu-baseline > "$OUT/ncu_light.log" 2>&1

@@ -74,10 +74,10 @@ class Clocks:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device: int):
+    def __init__(self, devices: str):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={self.Q}",
+            self.p = subprocess.Popen(["nvidia-smi", "-i", devices, f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "200"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except FileNotFoundError:
@@ -268,14 +268,16 @@ def run_ours(args):
         dev = e0.elapsed_time(e1) / 1e3
         return st, energy, dev, wall, qr_qsu
 
-    clocks = None
+    # one sampler on rank 0 for every GPU of the job, started before the
+    # warm-up so its start-up (driver queries) is over before the timed steps
+    class _NoClocks:
+        def stop(self):
+            return None
+
+    clocks = Clocks(",".join(str(i) for i in range(world))) if rank == 0 else _NoClocks()
     for i in range(args.warmup):
-        if i == args.warmup - 1:
-            clocks = Clocks(local)  # sampler start-up overlaps the last warm-up step, not the timed ones
         st, energy, _, _, _ = step()
         del st
-    if clocks is None:
-        clocks = Clocks(local)
     barrier()
     torch.cuda.synchronize()
     devs, walls, launches = [], [], 0

@@ -28,32 +28,71 @@ __device__ __forceinline__ double2 cmac2(const double2 u, const double2 a, const
     return r;
 }
 
+// In place (see dense1r): y-only partials, then y', then x'.
 template <int Q>
 __device__ __forceinline__ void dense1(double2 (&a)[16], const double2* __restrict__ m) {
     const double2 m00 = m[0], m01 = m[1], m10 = m[2], m11 = m[3];
+    const double n00 = -m00.y, n01 = -m01.y, n10 = -m10.y, n11 = -m11.y;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
         if ((r >> Q) & 1) continue;
         const int s = r | (1 << Q);
-        const double2 x = a[r], y = a[s];
-        a[r] = cmac2(m00, x, m01, y);
-        a[s] = cmac2(m10, x, m11, y);
+        asm("{\n"
+            ".reg .f64 p0, p1, p2, p3;\n"
+            "mul.rn.f64 p0, %5, %3;\n"       // x'.x <- m01.x y.x - m01.y y.y
+            "fma.rn.f64 p0, %4, %2, p0;\n"
+            "mul.rn.f64 p1, %6, %2;\n"       // x'.y <- m01.x y.y + m01.y y.x
+            "fma.rn.f64 p1, %4, %3, p1;\n"
+            "mul.rn.f64 p2, %8, %3;\n"       // y'.x <- m11.x y.x - m11.y y.y
+            "fma.rn.f64 p2, %7, %2, p2;\n"
+            "mul.rn.f64 p3, %9, %2;\n"       // y'.y <- m11.x y.y + m11.y y.x
+            "fma.rn.f64 p3, %7, %3, p3;\n"
+            "fma.rn.f64 p2, %13, %1, p2;\n"  // - m10.y x.y
+            "fma.rn.f64 p3, %12, %0, p3;\n"  // + m10.y x.x
+            "fma.rn.f64 %2, %11, %0, p2;\n"  // y'.x = m10.x x.x + ...
+            "fma.rn.f64 %3, %11, %1, p3;\n"  // y'.y = m10.x x.y + ...
+            "fma.rn.f64 p0, %15, %1, p0;\n"  // - m00.y x.y
+            "fma.rn.f64 p1, %14, %0, p1;\n"  // + m00.y x.x
+            "fma.rn.f64 %0, %10, %0, p0;\n"  // x'.x = m00.x x.x + ...
+            "fma.rn.f64 %1, %10, %1, p1;\n"  // x'.y = m00.x x.y + ...
+            "}\n"
+            : "+d"(a[r].x), "+d"(a[r].y), "+d"(a[s].x), "+d"(a[s].y)
+            : "d"(m01.x), "d"(n01), "d"(m01.y), "d"(m11.x), "d"(n11), "d"(m11.y), "d"(m00.x), "d"(m10.x),
+              "d"(m10.y), "d"(n10), "d"(m00.y), "d"(n00));
     }
 }
 
 // Dense 1-qubit gate whose first column is real (m00, m10 real): 6 fp64
 // operations per amplitude instead of 8.
+// In-place form: the y-only partial sums first, then y' and x' overwrite
+// their own registers, so every slot keeps its register across the op switch
+// (the C++ form left ~2 register copies per amplitude at the switch join).
 template <int Q>
 __device__ __forceinline__ void dense1r(double2 (&a)[16], const double2* __restrict__ m) {
     const double m00 = m[0].x, m10 = m[2].x;
     const double2 m01 = m[1], m11 = m[3];
+    const double n01 = -m01.y, n11 = -m11.y;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
         if ((r >> Q) & 1) continue;
         const int s = r | (1 << Q);
-        const double2 x = a[r], y = a[s];
-        a[r] = make_double2(fma(m00, x.x, fma(m01.x, y.x, -m01.y * y.y)), fma(m00, x.y, fma(m01.x, y.y, m01.y * y.x)));
-        a[s] = make_double2(fma(m10, x.x, fma(m11.x, y.x, -m11.y * y.y)), fma(m10, x.y, fma(m11.x, y.y, m11.y * y.x)));
+        asm("{\n"
+            ".reg .f64 p0, p1, p2, p3;\n"
+            "mul.rn.f64 p0, %5, %3;\n"
+            "fma.rn.f64 p0, %4, %2, p0;\n"
+            "mul.rn.f64 p1, %6, %2;\n"
+            "fma.rn.f64 p1, %4, %3, p1;\n"
+            "mul.rn.f64 p2, %11, %3;\n"
+            "fma.rn.f64 p2, %10, %2, p2;\n"
+            "mul.rn.f64 p3, %7, %2;\n"
+            "fma.rn.f64 p3, %10, %3, p3;\n"
+            "fma.rn.f64 %2, %9, %0, p2;\n"
+            "fma.rn.f64 %3, %9, %1, p3;\n"
+            "fma.rn.f64 %0, %8, %0, p0;\n"
+            "fma.rn.f64 %1, %8, %1, p1;\n"
+            "}\n"
+            : "+d"(a[r].x), "+d"(a[r].y), "+d"(a[s].x), "+d"(a[s].y)
+            : "d"(m01.x), "d"(n01), "d"(m01.y), "d"(m11.y), "d"(m00), "d"(m10), "d"(m11.x), "d"(n11));
     }
 }
 

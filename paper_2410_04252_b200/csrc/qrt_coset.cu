@@ -90,14 +90,49 @@ __device__ __forceinline__ double2 coset_one(const double2 (&a)[32], const doubl
     return acc;
 }
 
+// sum_rho T[rho] * Im(conj(a[r^XQ]) a[r]) (Im(w)-only groups, real coefficients).
+template <int XQ>
+__device__ __forceinline__ double coset_group_im(const double2 (&a)[32], const double2* __restrict__ T2) {
+    constexpr int H = top_bit(XQ);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+        const double2 t = T2[h];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int rho = 2 * h + u;
+            const int r = ins0(rho, H);
+            const int s = r ^ XQ;
+            const double2 A = a[s], B = a[r];
+            acc[rho & 3] = fma(u ? t.y : t.x, fma(A.x, B.y, -A.y * B.x), acc[rho & 3]);
+        }
+    }
+    return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
+// The single-bit groups of mask 1 << K: one_re[K] Re(w)-only, then one_im[K]
+// Im(w)-only (both real, 16-entry tables), then general ones (64 entries).
 template <int K>
 __device__ __forceinline__ void coset_ones(const double2 (&a)[32], const CosetParams& P, const CosetSet& S,
                                            const double* __restrict__ tabs, int& g, std::uint64_t W, std::uint64_t pe,
                                            double2& acc) {
-    const int n = S.one_cnt[K];
-    for (int i = 0; i < n; ++i, ++g) {
+    const int n = S.one_cnt[K], nre = S.one_re[K], nim = S.one_im[K];
+    const double2* __restrict__ t2 = reinterpret_cast<const double2*>(tabs);
+    for (int i = 0; i < nre; ++i, ++g) {
         const CosetGroup& G = P.groups[g];
-        const double2 r = coset_one<1 << K>(a, tabs + G.tab, G.mode);
+        const double r = coset_group<1 << K>(a, t2 + (G.tab >> 1));
+        const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
+        acc.x += odd ? -r : r;
+    }
+    for (int i = 0; i < nim; ++i, ++g) {
+        const CosetGroup& G = P.groups[g];
+        const double r = coset_group_im<1 << K>(a, t2 + (G.tab >> 1));
+        const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
+        acc.x += odd ? -r : r;
+    }
+    for (int i = nre + nim; i < n; ++i, ++g) {
+        const CosetGroup& G = P.groups[g];
+        const double2 r = coset_one<1 << K>(a, tabs + G.tab, 1);
         const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
         acc.x += odd ? -r.x : r.x;
         acc.y += odd ? -r.y : r.y;

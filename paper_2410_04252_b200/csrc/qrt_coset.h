@@ -45,6 +45,8 @@ struct CosetSet {
     std::uint32_t present;  // bit x: some fast group has mask x
     std::uint8_t xbeg[32];  // fast groups sorted by mask: [xbeg[x-1], xbeg[x]) have mask x
     std::uint8_t one_cnt[kCosetBits];  // then single-bit-mask groups: one_cnt[k] with mask 1 << k; generic after them
+    std::uint8_t one_re[kCosetBits];   // ... of which the first one_re[k] are mode 0 and the next one_im[k] mode 2
+    std::uint8_t one_im[kCosetBits];
 };
 
 // W = tile index (bits 0..11) | outer index of the CTA (bit 12 + i <-> outer axis i).

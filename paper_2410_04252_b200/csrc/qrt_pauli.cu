@@ -649,15 +649,6 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
         };
         // then the single-bit masks (linear passes; any table mode, evaluated
         // from the register coset), sorted by mask; the generic ones last
-        auto one_of = [&](const Sub& u) { return !fast_of(u) && __builtin_popcount(static_cast<unsigned>(u.xq)) == 1; };
-        auto cls = [&](const Sub& u) { return fast_of(u) ? 0 : one_of(u) ? 1 : 2; };
-        std::stable_sort(subs.begin(), subs.end(), [&](const Sub& a, const Sub& b) {
-            const int ca = cls(a), cb = cls(b);
-            if (ca != cb) return ca < cb;
-            return ca < 2 && a.xq < b.xq;
-        });
-        // emit in chunks that fit the launch parameters (a set whose
-        // subgroups overflow one launch is repeated with the same Q)
         auto re_real_of = [&](const Sub& u) {
             for (int t : u.terms)
                 if ((__builtin_popcountll(y[t]) & 1) || coeffs[2 * t + 1] != 0.0) return false;
@@ -668,6 +659,20 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
                 if (!(__builtin_popcountll(y[t]) & 1) || coeffs[2 * t + 1] != 0.0) return false;
             return true;
         };
+        auto one_of = [&](const Sub& u) { return !fast_of(u) && __builtin_popcount(static_cast<unsigned>(u.xq)) == 1; };
+        auto cls = [&](const Sub& u) { return fast_of(u) ? 0 : one_of(u) ? 1 : 2; };
+        // single-bit groups of one mask: Re(w)-only real (mode 0) first, then
+        // Im(w)-only real (mode 2), then general, so the kernel walks each
+        // run with a fixed body
+        auto one_mode = [&](const Sub& u) { return re_real_of(u) ? 0 : im_real_of(u) ? 1 : 2; };
+        std::stable_sort(subs.begin(), subs.end(), [&](const Sub& a, const Sub& b) {
+            const int ca = cls(a), cb = cls(b);
+            if (ca != cb) return ca < cb;
+            if (ca == 1 && a.xq == b.xq) return one_mode(a) < one_mode(b);
+            return ca < 2 && a.xq < b.xq;
+        });
+        // emit in chunks that fit the launch parameters (a set whose
+        // subgroups overflow one launch is repeated with the same Q)
         std::size_t at = 0;
         while (at < subs.size()) {
             auto room = [&](std::size_t from) {
@@ -706,6 +711,14 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
                 int cnt = 0;
                 for (std::size_t q = at; q < end; ++q) cnt += one_of(subs[q]) && subs[q].xq == (1 << k);
                 Sc.one_cnt[k] = static_cast<std::uint8_t>(cnt);  // single-bit subgroups, after the fast ones
+                int nre = 0, nim = 0;
+                for (std::size_t q = at; q < end; ++q)
+                    if (one_of(subs[q]) && subs[q].xq == (1 << k)) {
+                        nre += one_mode(subs[q]) == 0;
+                        nim += one_mode(subs[q]) == 1;
+                    }
+                Sc.one_re[k] = static_cast<std::uint8_t>(nre);
+                Sc.one_im[k] = static_cast<std::uint8_t>(nim);
             }
             for (std::size_t q = at; q < end; ++q) {
                 const Sub& u = subs[q];

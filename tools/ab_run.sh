@@ -1,6 +1,5 @@
-# scratch: final 1-GPU checks + profile round
-O=gpurun_out/final2; mkdir -p $O
-timeout 1500 python -m pytest tests -m gpu -x -q > $O/gputests.log 2>&1; echo rc=$? >> $O/gputests.log
-python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo rc=$? >> $O/smoke.log
-OUT=$O/prof bash tools/profile_round.sh > $O/prof.log 2>&1
-python bench.py --impl reference > $O/bench_ref.json 2> $O/bench_ref.err
+# scratch: single-bit EVC bodies split by table mode
+O=gpurun_out/ab19; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_evc.py -x -q > $O/tests.log 2>&1; echo rc=$? >> $O/tests.log
+python bench.py --no-cpu-baseline --warmup 1 --steps 2 --circuit hea --hamiltonian uniform --terms 1000 > $O/uni.json 2>&1
+python bench.py --no-cpu-baseline --warmup 1 --steps 2 --circuit hea > $O/hea.json 2>&1

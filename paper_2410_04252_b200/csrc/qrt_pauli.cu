@@ -1096,14 +1096,22 @@ PauliPlanHost build_pauli_plan(int nl, int pe_begin, int n_terms, const std::uin
     if (linear && !wide.empty()) {
         std::vector<std::size_t> pending(wide.size());
         for (std::size_t i = 0; i < wide.size(); ++i) pending[i] = i;
-        const std::uint64_t coal_m = (1ull << coal) - 1;
+        // unit low positions of a linear tile: 2 (64-byte runs; 10 groups per
+        // pass, measured faster than 4 positions / 256-byte runs with 8 groups:
+        // the passes are compute-bound).  QRT_EVC_LINEAR_COAL overrides (2..4;
+        // fewer would not fit the pipelined kernel's shared memory).
+        const int lcoal = [&] {
+            const char* e = std::getenv("QRT_EVC_LINEAR_COAL");
+            return std::max(std::min(coal, 2), std::min(coal, e ? std::atoi(e) : 2));
+        }();
+        const std::uint64_t coal_m = (1ull << lcoal) - 1;
         std::vector<std::uint64_t> smL(static_cast<std::size_t>(n_terms), 0);
         while (!pending.empty()) {
             std::vector<std::uint64_t> basis;
             std::vector<int> piv;
             std::vector<std::size_t> batch, rest;
             for (std::size_t w : pending) {
-                if (static_cast<int>(batch.size()) == T - coal) {
+                if (static_cast<int>(batch.size()) == T - lcoal) {
                     rest.push_back(w);
                     continue;
                 }
@@ -1125,7 +1133,7 @@ PauliPlanHost build_pauli_plan(int nl, int pe_begin, int n_terms, const std::uin
                 cols[piv[k]] = wide[batch[k]].first;
                 B |= 1ull << piv[k];
             }
-            for (int p = coal; p < nl && popc(B) < T; ++p) B |= 1ull << p;
+            for (int p = lcoal; p < nl && popc(B) < T; ++p) B |= 1ull << p;
             std::vector<std::pair<std::uint64_t, std::vector<int>>> fl;
             std::vector<int> gi;
             for (std::size_t k = 0; k < batch.size(); ++k) {

@@ -420,16 +420,16 @@ __global__ void __launch_bounds__(256) norm_kernel(const amp_t* __restrict__ v, 
 int popc(std::uint64_t v) { return __builtin_popcountll(v); }
 
 // Gathers `local` (2 doubles per owned PE) into `all` (2 doubles per PE).
+// `d_local` sits in the reduction buffer, which callers size with 2·p
+// further doubles behind it: the all-gather lands there, so no
+// per-call stream-ordered allocation sits between the EVC kernels.
 void gather_partials(qrt_state* st, const double* d_local, double* all) {
     const std::size_t per = 2 * static_cast<std::size_t>(st->pe_count);
     if (st->comm && st->comm->world > 1) {
-        double* buf = nullptr;
-        QRT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), 2 * static_cast<std::size_t>(st->p) * sizeof(double),
-                                 st->stream));
+        double* buf = const_cast<double*>(d_local) + per;
         QRT_NCCL(ncclAllGather(d_local, buf, per, ncclDouble, st->comm->nccl, st->stream));
         QRT_CUDA(cudaMemcpyAsync(all, buf, 2 * static_cast<std::size_t>(st->p) * sizeof(double), cudaMemcpyDeviceToHost,
                                  st->stream));
-        QRT_CUDA(cudaFreeAsync(buf, st->stream));
         QRT_CUDA(cudaStreamSynchronize(st->stream));
     } else {
         QRT_CUDA(cudaMemcpyAsync(all + 2 * static_cast<std::size_t>(st->pe_begin), d_local, per * sizeof(double),
@@ -1245,7 +1245,7 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
 
     const int ctas = 1 << (nl - T);
     const std::size_t slots = static_cast<std::size_t>(ctas) * static_cast<std::size_t>(st->pe_count);
-    double* red = ensure_red(st, 2 * slots + 2 * static_cast<std::size_t>(st->pe_count));
+    double* red = ensure_red(st, 2 * slots + 2 * static_cast<std::size_t>(st->pe_count) + 2 * static_cast<std::size_t>(st->p));
     double* out = red + 2 * slots;
     QRT_CUDA(cudaMemsetAsync(red, 0, 2 * slots * sizeof(double), st->stream));
 
@@ -1344,7 +1344,7 @@ void pauli_plan_info(int nl, int n_terms, const std::uint64_t* x, const std::uin
 double norm(qrt_state* st) {
     const int blocks = 148 * 4;
     const std::size_t slots = static_cast<std::size_t>(blocks) * static_cast<std::size_t>(st->pe_count);
-    double* red = ensure_red(st, 2 * slots + 2 * static_cast<std::size_t>(st->pe_count));
+    double* red = ensure_red(st, 2 * slots + 2 * static_cast<std::size_t>(st->pe_count) + 2 * static_cast<std::size_t>(st->p));
     double* out = red + 2 * slots;
     for (int i = 0; i < st->pe_count; ++i) {
         norm_kernel<<<blocks, 256, 0, st->stream>>>(st->live(i), st->amps, red + 2 * static_cast<std::size_t>(i) * blocks);

@@ -1,11 +1,14 @@
 #!/usr/bin/env python
 """One VQE iteration (QSU + QR + EVC) of arXiv 2410.04252 on B200.
 
-Workload (BASELINE.json configs[1], "C2"): GateFabric, n=30 qubits, layers=4n=120
-(1,680 dense 4-qubit blocks, Rng seed 1), lazy flat_tiling schedule, then EVC
-of the synthetic Jordan-Wigner Hamiltonian gen_synthetic_jw(30, 1, max_span=10)
-with diagonalization.  At N GPUs the same 30-qubit state is sharded 2^g-way
-(p = N, strong scaling); the schedule's QRs move amplitudes over NVLink.
+Workload (BASELINE.json configs[2], "C3" — the metric is quoted at 32-34
+qubits and 32 qubits is the largest config that fits one GPU): GateFabric,
+n=32 qubits, layers=4n=128 (1,920 dense 4-qubit blocks, Rng seed 1), lazy
+flat_tiling schedule, then EVC of the synthetic Jordan-Wigner Hamiltonian
+gen_synthetic_jw(32, 1, max_span=10) (8,994 strings) with diagonalization.
+At N GPUs the same 32-qubit state (64 GiB) is sharded 2^g-way (p = N, strong
+scaling, C3's "1/2/4/8 B200"); the schedule's QRs move amplitudes over NVLink.
+--qubits 30 gives C2, --circuit hea --qubits 34 C4, --hamiltonian uniform C5.
 
 A step = init_state + run_qsu + expectation through the public API
 (= evaluate_energy, dist_sim.cpp:357-363).  `value` is the step's device time
@@ -45,7 +48,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--qubits", type=int, default=30)
+    ap.add_argument("--qubits", type=int, default=32,
+                    help="32 = C3, the metric's configuration (64 GiB state on one GPU); 30 = C2; 34 = C4/C5")
     ap.add_argument("--circuit", choices=["gatefabric", "hea"], default="gatefabric",
                     help="gatefabric (C2/C3) or the hardware-efficient ansatz (C4)")
     ap.add_argument("--layers", type=int, default=0, help="default 4n for GateFabric (PAPER.md:958), 20 for HEA")
@@ -112,17 +116,6 @@ def dist_env():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
-def uniform_terms(qb, n, count, seed=2024):
-    """C5 stress Hamiltonian: letters "IXYZ"[u], coefficients
-    U(-1, 1), from numpy's PCG64(2024) (the reference has no such generator)."""
-    import numpy as np
-
-    rng = np.random.default_rng(seed)
-    letters = rng.integers(0, 4, size=(count, n))
-    coeffs = rng.uniform(-1.0, 1.0, size=count)
-    return [qb.PauliTerm(complex(c, 0.0), "".join("IXYZ"[v] for v in row)) for row, c in zip(letters, coeffs)]
-
-
 def workload(qb, args, p):
     n = args.qubits
     if args.circuit == "hea":
@@ -135,55 +128,113 @@ def workload(qb, args, p):
     shape = qb.ClusterShape.flat(p)
     sched = {"flat": qb.flat_tiling, "hierarchical": qb.hierarchical_tiling, "adhoc": qb.adhoc_schedule}[args.schedule](
         circuit, deps, shape)
-    terms = qb.gen_synthetic_jw(n, 1, args.span) if args.hamiltonian == "jw" else uniform_terms(qb, n, args.terms)
+    terms = (qb.gen_synthetic_jw(n, 1, args.span) if args.hamiltonian == "jw"
+             else qb.gen_uniform_words(n, args.terms, 2024))
     plan = qb.plan_evc(terms, n, shape, True, 8)
     return n, layers, circuit, sched, terms, plan, shape
 
 
 def config_of(args, n, layers, n_gates, n_terms, p, qr_qsu=None, qr_evc=None):
-    circ = (f"C2 GateFabric {n}q layers={layers} ({n_gates} dense 4q gates, seed 1)" if args.circuit == "gatefabric"
+    cfg = {30: "C2", 32: "C3", 34: "C4/C5"}.get(n, "custom")
+    circ = (f"{cfg} GateFabric {n}q layers={layers} ({n_gates} dense 4q gates, seed 1)" if args.circuit == "gatefabric"
             else f"C4 HEA {n}q depth={layers} ({n_gates} gates: RY dense, RZ/CZ diagonal, seed 1)")
     ham = (f"gen_synthetic_jw({n},1,max_span={args.span})" if args.hamiltonian == "jw"
-           else f"uniform random words (PCG64 2024)")
-    return {"workload": f"{circ} + EVC of {ham} ({n_terms} Pauli strings), {args.schedule} schedule, p={p}",
+           else "C5 stress: uniform words IXYZ[Rng(2024).below(4)]")
+    sched = {"flat": "lazy (flat_tiling)", "hierarchical": "lazy (hierarchical_tiling)",
+             "adhoc": "eager (adhoc_schedule)"}[args.schedule]
+    return {"workload": f"{circ} + EVC of {ham} ({n_terms} Pauli strings), {sched} schedule, p={p}",
             "qubits": n, "pes": p, "schedule": args.schedule, "qr_qsu": qr_qsu, "qr_evc": qr_evc,
             "l2": "inputs larger than L2 (state 16 B x 2^n)", "parallelism": f"state sharded {p}-way"}
 
 
-def cpu_baseline(args, n, p, n_gates, n_terms, layers):
-    """Reference CPU path (oracle/_ref, the unmodified reference) on a bounded
-    sample: an n_s-qubit state, the first gates of the circuit (6 GateFabric
-    blocks, or one HEA layer) + 24 strings, scaled linearly in 2^n."""
+def reference_counts(args, p):
+    """Gate, string and QR counts of the full-size workload from the reference
+    itself (oracle/_ref): its generators, its scheduler (qsu_scheduler.cpp) and
+    its EVC planner (evc_scheduler.cpp); the EVC QRs are re-derived from the
+    post-QSU layout exactly as expectation() does (dist_sim.cpp:268-271)."""
+    from oracle import ref as R
+
+    n = args.qubits
+    if args.circuit == "hea":
+        layers = args.layers or 20
+        circ = R.Circuit.hea(n, layers, 1)
+    else:
+        layers = args.layers or 4 * n
+        circ = R.Circuit.gatefabric(n, layers, 1, False)
+    arity, _, _ = circ.export()
+    per_arity = [int((arity == a).sum()) for a in (1, 2, 3, 4)]
+    terms = R.Terms.jw(n, 1, args.span) if args.hamiltonian == "jw" else R.Terms.uniform(n, args.terms, 2024)
+    ks = []
+    qr_qsu = qr_evc = 0
+    nl = n - (p.bit_length() - 1)
+    locals_ = (1 << nl) - 1
+    if p > 1:
+        d = circ.schedule(args.schedule, p)
+        for ev in d["events"]:
+            new = sum(1 << q for q, pos in enumerate(ev["after_pos_of"]) if pos < nl)
+            ks.append(bin(new & ~locals_).count("1"))
+            locals_ = new
+        qr_qsu = len(ks)
+        plan = terms.plan(n, p, 0, 0, True, 8)
+        for tile in plan["plan"]["tiles"]:
+            new = sum(1 << q for q in tile["local_qubits"])
+            if new != locals_:
+                ks.append(bin(new & ~locals_).count("1"))
+                locals_ = new
+                qr_evc += 1
+    return {"n": n, "layers": layers, "per_arity": per_arity, "n_gates": circ.m, "n_terms": terms.count,
+            "qr_k": ks, "qr_qsu": qr_qsu, "qr_evc": qr_evc}
+
+
+def cpu_baseline(args, p, counts=None):
+    """The reference's own CPU path (oracle/_ref = the unmodified reference
+    library) on SURVEY.md §8d's bounded sample: at n_s qubits and the same p,
+    the first 16 gates of each arity through apply_gate_narrow, the first 64
+    strings through expectation, one perform_qr per k — then extrapolated
+    linearly to the full workload (per-gate / per-string / per-QR cost scales as
+    2^n at fixed k).  Threads: workers = nproc, of which the reference itself
+    uses min(workers, p) (dist_sim.cpp:25); perform_qr is single-threaded.
+    Never imports the product."""
     from oracle import ref as R
 
     if not R.available():
         return None
-    import multiprocessing
-
-    import paper_2410_04252_b200 as qb
-
+    nproc = os.cpu_count() or 1
+    counts = counts or reference_counts(args, p)
+    n = counts["n"]
     ns = min(args.cpu_sample_qubits, n)
-    workers = min(p, multiprocessing.cpu_count())
     if args.circuit == "hea":
-        circ = R.Circuit.from_product(qb.gen_hea(ns, 1, 1, True))
-        n_sample = 3 * ns - 1
+        circ = R.Circuit.hea(ns, 1, 1)
     else:
         circ = R.Circuit.gatefabric(ns, 4, 1, True)
-        n_sample = 6
-    if args.hamiltonian == "jw":
-        terms = R.Terms.jw(ns, 1, args.span)
-    else:
-        terms = R.Terms.from_product(uniform_terms(qb, ns, 64), ns)
+    terms = R.Terms.jw(ns, 1, args.span) if args.hamiltonian == "jw" else R.Terms.uniform(ns, 4096, 2024)
     t0 = time.time()
-    g, t = R.time_sample(circ, terms, p, workers, n_sample, 24)
+    g, t, q = R.time_prefix(circ, terms, p, nproc, 16, 64)
     wall = time.time() - t0
     scale = float(1 << (n - ns))
-    per_iter = (g * n_gates + t * n_terms) * scale
-    return {"value": per_iter, "unit": "s", "cores": workers, "kind": "reference",
-            "sample": f"reference dist_sim (oracle/_ref) apply_gate_narrow x{n_sample} + expectation x24 strings at "
-                      f"n={ns}, p={p}, workers={workers} ({wall:.1f} s of CPU work); per-gate {g:.3g} s and "
-                      f"per-string {t:.3g} s scaled by 2^{n - ns} to {n_gates} gates + {n_terms} strings "
-                      f"(extrapolated, linear in 2^n)"}
+    gates_s = sum(c * s for c, s in zip(counts["per_arity"], g)) * scale
+    evc_s = counts["n_terms"] * t * scale
+    qr_s = sum(q[k - 1] for k in counts["qr_k"]) * scale
+    per_iter = gates_s + evc_s + qr_s
+    return {"value": per_iter, "unit": "s", "cores": min(nproc, p), "nproc": nproc, "workers": nproc,
+            "kind": "reference",
+            "phases_s": {"gates": gates_s, "evc": evc_s, "qr": qr_s},
+            "counts": counts,
+            "sample": f"reference dist_sim (oracle/_ref): first 16 gates per arity (apply_gate_narrow), 64 strings "
+                      f"(expectation), one perform_qr per k at n={ns}, p={p}, workers={nproc} (the reference uses "
+                      f"min(workers, p) = {min(nproc, p)} threads; QR 1 thread); {wall:.1f} s of CPU work. "
+                      f"Per-gate s by arity {[round(x, 4) for x in g]}, per-string {t:.4g} s, per-QR s by k "
+                      f"{[round(x, 4) for x in q]}; scaled by 2^{n - ns} to {counts['n_gates']} gates + "
+                      f"{counts['n_terms']} strings + {len(counts['qr_k'])} QRs (extrapolated, linear in 2^n)"}
+
+
+def loaded_native():
+    """In-tree shared objects mapped into this process (reference arm: oracle/_ref only)."""
+    try:
+        maps = open("/proc/self/maps").read().splitlines()
+    except OSError:
+        return []
+    return sorted({m.split()[-1] for m in maps if m.endswith(".so") and str(ROOT) in m})
 
 
 def run_reference(args):
@@ -191,24 +242,16 @@ def run_reference(args):
     if rank != 0:
         return 0
     from oracle import ref as R
-    import paper_2410_04252_b200 as qb  # host-only use: generators + counts for the config echo
 
     p = max(1, world)
-    n = args.qubits
-    layers = args.layers or 4 * n
-    if args.circuit == "hea":
-        layers = args.layers or 20
-        n_gates = layers * (3 * n - 1)
-    else:
-        n_gates = qb.gatefabric_block_count(n, layers)
-    n_terms = int(qb.synthetic_jw_term_count(n, args.span)) if args.hamiltonian == "jw" else args.terms
     if not R.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libqrtile_ref.so not built"}))
         return 0
+    counts = reference_counts(args, p)
     vals = []
     base = None
     for i in range(args.warmup + args.steps):
-        base = cpu_baseline(args, n, p, n_gates, n_terms, layers)
+        base = cpu_baseline(args, p, counts)
         if i >= args.warmup:
             vals.append(base["value"])
     v = statistics.median(vals)
@@ -216,8 +259,11 @@ def run_reference(args):
     line = {"metric": "VQE iteration time (QSU+EVC)", "value": v, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference", "config": config_of(args, n, layers, n_gates, n_terms, p),
-            "cpu_baseline": base, "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "impl": "reference",
+            "config": config_of(args, counts["n"], counts["layers"], counts["n_gates"], counts["n_terms"], p,
+                                counts["qr_qsu"], counts["qr_evc"]),
+            "cpu_baseline": base, "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "native_so_loaded": loaded_native()}
     print(json.dumps(line))
     return 0
 
@@ -275,8 +321,13 @@ def run_ours(args):
             return None
 
     clocks = Clocks(",".join(str(i) for i in range(world))) if rank == 0 else _NoClocks()
+    # warm-up; the last warm-up step is the profiled one (per-kernel-family CUDA
+    # events for the roofline), so no extra step is needed after the timed ones
+    stats = None
     for i in range(args.warmup):
-        st, energy, _, _, _ = step()
+        st, energy, _, _, _ = step(profile=(i == args.warmup - 1))
+        if i == args.warmup - 1:
+            stats = st.stats()
         del st
     barrier()
     torch.cuda.synchronize()
@@ -296,10 +347,10 @@ def run_ours(args):
     dev_t = max_over_ranks(statistics.mean(devs))
     wall_t = max_over_ranks(statistics.mean(walls))
 
-    # one extra profiled (untimed) step: per-kernel-family event times for the roofline
-    st, _, _, _, _ = step(profile=True)
-    stats = st.stats()
-    del st
+    if stats is None:  # --warmup 0: profile one extra untimed step
+        st, _, _, _, _ = step(profile=True)
+        stats = st.stats()
+        del st
     g, qr, pa = stats["gates"], stats["qr"], stats["pauli"]
     fam_kernel = {"gates": ("gate_pass_kernel (DMMA fp64 tensor, dense 3/4-qubit gates)" if args.circuit == "gatefabric"
                             else "light_pass_kernel (register-resident 1q/2q/diagonal runs)"),
@@ -371,8 +422,9 @@ def run_ours(args):
                       "gate_passes": g["launches"], "qr_launches": qr["launches"], "pauli_passes": pa["launches"],
                       "qr_nvlink_gbs": (qr["bytes"] / (qr["ms"] / 1e3) / 1e9) if qr["ms"] > 0 else None},
     }
-    if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args, n, p, n_gates, n_terms, layers)
+    line["native_so_loaded"] = loaded_native()
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, p)
     print(json.dumps(line))
     return 0
 

@@ -29,10 +29,12 @@ def lib() -> C.CDLL:
         for name, args in {
             "ref_circuit_gatefabric": [C.c_int, C.c_int, C.c_uint64, C.c_int],
             "ref_circuit_random": [C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int],
+            "ref_circuit_hea": [C.c_int, C.c_int, C.c_uint64],
             "ref_circuit_fixture": [C.c_char_p, C.c_uint64],
             "ref_circuit_from_arrays": [C.c_int, C.c_int, P(C.c_int), P(C.c_int), P(C.c_double)],
             "ref_terms_jw": [C.c_int, C.c_uint64, C.c_int],
             "ref_terms_fixture": [C.c_char_p],
+            "ref_terms_uniform": [C.c_int, C.c_int, C.c_uint64],
             "ref_terms_from_arrays": [C.c_int, C.c_int, C.c_char_p, P(C.c_double)],
         }.items():
             getattr(L, name).argtypes = args
@@ -61,6 +63,8 @@ def lib() -> C.CDLL:
                                       P(C.c_double), P(C.c_int), P(C.c_double)]
         L.ref_evaluate_energy.argtypes = [vp, vp, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                           P(C.c_double), P(C.c_int), P(C.c_int)]
+        L.ref_time_prefix.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, P(C.c_double), P(C.c_double),
+                                      P(C.c_double)]
         L.ref_time_sample.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, P(C.c_double), P(C.c_double)]
         _LIB = L
     return _LIB
@@ -97,6 +101,15 @@ class Circuit:
     @classmethod
     def gatefabric(cls, n, layers, seed=1, payloads=True):
         return cls(lib().ref_circuit_gatefabric(n, layers, seed, int(payloads)))
+
+    @classmethod
+    def hea(cls, n, depth, seed=1):
+        """SURVEY.md §8d C4 HEA built from reference types (ref_shim.cpp)."""
+        return cls(lib().ref_circuit_hea(n, depth, seed))
+
+    @property
+    def m(self):
+        return lib().ref_circuit_m(self.h)
 
     @classmethod
     def random(cls, n, m, seed, max_arity=2, payloads=True):
@@ -157,6 +170,10 @@ class Circuit:
 
 
 class Terms:
+    @property
+    def count(self):
+        return lib().ref_terms_count(self.h)
+
     def __init__(self, handle):
         if not handle:
             raise RuntimeError("reference: " + lib().ref_last_error().decode())
@@ -173,6 +190,10 @@ class Terms:
     @classmethod
     def fixture(cls, name):
         return cls(lib().ref_terms_fixture(name.encode()))
+
+    @classmethod
+    def uniform(cls, n, count, seed=2024):
+        return cls(lib().ref_terms_uniform(n, count, seed))
 
     @classmethod
     def from_product(cls, terms, n):
@@ -228,3 +249,14 @@ def time_sample(circ: Circuit, terms: Terms | None, p, workers, n_gates, n_terms
     _check(lib().ref_time_sample(circ.h, terms.h if terms else None, p, workers, n_gates, n_terms, C.byref(g),
                                  C.byref(t)))
     return g.value, t.value
+
+
+def time_prefix(circ: Circuit, terms: Terms | None, p, workers, per_arity=16, n_terms=64):
+    """SURVEY.md §8d bounded sample: seconds per gate of each arity 1..4, per
+    string, and per perform_qr of k = 1..log2 p (ref_shim.cpp ref_time_prefix)."""
+    g = np.zeros(4)
+    q = np.zeros(max(1, p.bit_length() - 1))
+    t = C.c_double(0)
+    _check(lib().ref_time_prefix(circ.h, terms.h if terms else None, p, workers, per_arity, n_terms, _d(g),
+                                 C.byref(t), _d(q)))
+    return g.tolist(), t.value, q.tolist()[: p.bit_length() - 1]

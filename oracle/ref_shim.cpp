@@ -85,6 +85,50 @@ void* ref_circuit_gatefabric(int n, int layers, uint64_t seed, int payloads) {
     return c;
 }
 
+// The HEA of SURVEY.md §8d C4 (absent from the reference): per layer RY(theta)
+// on every qubit, RZ(theta) on every qubit, CZ(q, q+1) for even q then odd q,
+// theta ~ uniform(0, 2 pi) from the reference's Rng(seed) in gate order —
+// built from reference types so the reference arm never loads the product.
+void* ref_circuit_hea(int n, int depth, uint64_t seed) {
+    Circuit* c = nullptr;
+    guarded([&] {
+        auto out = std::make_unique<Circuit>();
+        out->n = n;
+        Rng rng(seed);
+        auto angle = [&] { return rng.uniform(0.0, 2.0 * 3.14159265358979323846); };
+        auto push = [&](std::vector<int> t, GatePayload pl) {
+            out->operators.push_back(make_gate(static_cast<int>(out->operators.size()), std::move(t), std::move(pl)));
+        };
+        auto cz = std::make_shared<GateMatrix>(4);
+        cz->at(0, 0) = 1.0;
+        cz->at(1, 1) = 1.0;
+        cz->at(2, 2) = 1.0;
+        cz->at(3, 3) = -1.0;
+        for (int layer = 0; layer < depth; ++layer) {
+            for (int q = 0; q < n; ++q) {
+                const double th = angle();
+                auto m = std::make_shared<GateMatrix>(2);
+                m->at(0, 0) = std::cos(th / 2);
+                m->at(0, 1) = -std::sin(th / 2);
+                m->at(1, 0) = std::sin(th / 2);
+                m->at(1, 1) = std::cos(th / 2);
+                push({q}, m);
+            }
+            for (int q = 0; q < n; ++q) {
+                const double th = angle();
+                auto m = std::make_shared<GateMatrix>(2);
+                m->at(0, 0) = std::polar(1.0, -th / 2);
+                m->at(1, 1) = std::polar(1.0, th / 2);
+                push({q}, m);
+            }
+            for (int parity = 0; parity < 2; ++parity)
+                for (int q = parity; q + 1 < n; q += 2) push({q, q + 1}, cz);
+        }
+        c = out.release();
+    });
+    return c;
+}
+
 void* ref_circuit_random(int n, int m, uint64_t seed, int max_arity, int payloads) {
     Circuit* c = nullptr;
     guarded([&] { c = new Circuit(gen_random_circuit(n, m, seed, max_arity, payloads != 0)); });
@@ -157,6 +201,23 @@ void* ref_terms_jw(int n, uint64_t seed, int max_span) {
     Terms* t = nullptr;
     guarded([&] {
         t = new Terms{n, gen_synthetic_jw(n, seed, max_span)};
+    });
+    return t;
+}
+// C5 stress words drawn with the reference's own Rng
+// (models.hpp:15-31, models.cpp:26-35): letters "IXYZ"[below(4)] per qubit,
+// then the coefficient uniform(-1, 1).
+void* ref_terms_uniform(int n, int count, uint64_t seed) {
+    Terms* t = nullptr;
+    guarded([&] {
+        Rng rng(seed);
+        std::vector<PauliTerm> ts;
+        for (int i = 0; i < count; ++i) {
+            std::string letters(static_cast<std::size_t>(n), 'I');
+            for (int q = 0; q < n; ++q) letters[static_cast<std::size_t>(q)] = "IXYZ"[rng.below(4)];
+            ts.push_back(PauliTerm{Amp{rng.uniform(-1.0, 1.0), 0.0}, letters});
+        }
+        t = new Terms{n, std::move(ts)};
     });
     return t;
 }
@@ -393,6 +454,75 @@ int ref_time_sample(void* circ, void* terms, int p, int workers, int n_gates, in
             (void)expectation(st, plan, pick_terms, workers);
             double t3 = secs();
             *sec_per_term = pick_terms.empty() ? 0.0 : (t3 - t2) / static_cast<double>(pick_terms.size());
+        }
+    });
+}
+
+// The reference arm's bounded sample (SURVEY.md §8d "CPU timing beside it"):
+// on an identity-layout state of circ->n qubits and flat(p), time
+//   * apply_gate_narrow (dist_sim.cpp:163-201) on the first `per_arity`
+//     narrow gates of each arity 1..4 -> sec_per_gate[arity-1] (0 if none),
+//   * expectation (dist_sim.cpp:263-300) on the first `n_terms` terms that
+//     need no QR under the identity layout -> *sec_per_term,
+//   * perform_qr (dist_sim.cpp:203-240; single-threaded) once for each k in
+//     1..log2 p, swapping the k highest local qubits with the k globals ->
+//     sec_per_qr[k-1].
+int ref_time_prefix(void* circ, void* terms, int p, int workers, int per_arity, int n_terms,
+                    double* sec_per_gate, double* sec_per_term, double* sec_per_qr) {
+    return guarded([&] {
+        auto* c = static_cast<Circuit*>(circ);
+        ClusterShape s = ClusterShape::flat(p);
+        DistributedState st = init_state(c->n, s);
+        for (int a = 1; a <= 4; ++a) {
+            int done = 0;
+            double t0 = secs();
+            for (auto& op : c->operators) {
+                if (done >= per_arity) break;
+                if (op.arity() != a || classify_access(op, st.layout) != Access::Narrow) continue;
+                apply_gate_narrow(st, op, workers);
+                ++done;
+            }
+            sec_per_gate[a - 1] = done ? (secs() - t0) / done : 0.0;
+        }
+        *sec_per_term = 0.0;
+        if (terms && n_terms > 0) {
+            auto& all = static_cast<Terms*>(terms)->terms;
+            std::vector<PauliTerm> pick_terms;
+            for (auto& t : all) {
+                bool ok = true;
+                for (int q = 0; q < t.n(); ++q) {
+                    char ch = t.letters[static_cast<std::size_t>(q)];
+                    if (ch != 'I' && ch != 'Z' && st.layout.pos_of[static_cast<std::size_t>(q)] >= st.layout.n_local) ok = false;
+                }
+                if (ok) pick_terms.push_back(t);
+                if (static_cast<int>(pick_terms.size()) >= n_terms) break;
+            }
+            PauliTilePlan plan;
+            plan.n = c->n;
+            plan.n_local = st.layout.n_local;
+            plan.shape = s;
+            plan.diagonalized = true;
+            PauliTile tile;
+            tile.local_qubits = st.layout.local_set();
+            for (int i = 0; i < static_cast<int>(pick_terms.size()); ++i) tile.terms.push_back(i);
+            plan.tiles.push_back(tile);
+            double t2 = secs();
+            (void)expectation(st, plan, pick_terms, workers);
+            double t3 = secs();
+            *sec_per_term = pick_terms.empty() ? 0.0 : (t3 - t2) / static_cast<double>(pick_terms.size());
+        }
+        const int g = s.global_bits();
+        for (int k = 1; k <= g; ++k) {
+            QubitSet locals = st.layout.local_set();
+            const int nl = st.layout.n_local;
+            for (int j = 0; j < k; ++j) {
+                locals &= ~(QubitSet{1} << st.layout.qubit_at[static_cast<std::size_t>(nl - 1 - j)]);
+                locals |= QubitSet{1} << st.layout.qubit_at[static_cast<std::size_t>(nl + j)];
+            }
+            auto ev = make_qr_event(st.layout, locals);
+            double t0 = secs();
+            if (ev) perform_qr(st, *ev);
+            sec_per_qr[k - 1] = secs() - t0;
         }
     });
 }

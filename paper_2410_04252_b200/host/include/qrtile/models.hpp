@@ -47,6 +47,11 @@ int gatefabric_block_count(int n, int layers);
 std::vector<PauliTerm> gen_synthetic_jw(int n, std::uint64_t seed, int max_span = 0);
 std::uint64_t synthetic_jw_term_count(int n, int max_span = 0);
 
+// C5 stress Hamiltonian: per word, letters "IXYZ"[rng.below(4)]
+// for q = 0..n-1 (the letter draw of acceptance.cpp:251 / test_evc_scheduler.cpp:133
+// over the whole word), then coefficient rng.uniform(-1, 1); one Rng(seed) stream.
+std::vector<PauliTerm> gen_uniform_words(int n, int count, std::uint64_t seed);
+
 Circuit gen_random_circuit(int n, int m, std::uint64_t seed, int max_arity = 2, bool payloads = true);
 ReferenceState random_state(int n, std::uint64_t seed);
 

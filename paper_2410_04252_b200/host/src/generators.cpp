@@ -221,6 +221,20 @@ Circuit gen_hea(const HeaSpec& spec) {
     return c;
 }
 
+std::vector<PauliTerm> gen_uniform_words(int n, int count, std::uint64_t seed) {
+    if (n < 1) throw ConfigError("uniform words need at least 1 qubit");
+    if (count < 0) throw ConfigError("uniform word count must be non-negative");
+    Rng rng(seed);
+    std::vector<PauliTerm> terms;
+    terms.reserve(static_cast<std::size_t>(count));
+    for (int t = 0; t < count; ++t) {
+        std::string letters(static_cast<std::size_t>(n), 'I');
+        for (int q = 0; q < n; ++q) letters[static_cast<std::size_t>(q)] = "IXYZ"[rng.below(4)];
+        terms.push_back(PauliTerm{Amp{rng.uniform(-1.0, 1.0), 0.0}, std::move(letters)});
+    }
+    return terms;
+}
+
 // ---------------------------------------------------------------- fixtures
 
 std::vector<std::string> fixture_circuit_names() { return {"fig2", "fig3", "fig7", "gatefabric-fig6"}; }

@@ -250,6 +250,7 @@ PYBIND11_MODULE(_qrtile, m) {
     }, py::arg("n"), py::arg("depth"), py::arg("seed") = 1, py::arg("payloads") = true);
     m.def("gen_synthetic_jw", &gen_synthetic_jw, py::arg("n"), py::arg("seed"), py::arg("max_span") = 0);
     m.def("synthetic_jw_term_count", &synthetic_jw_term_count, py::arg("n"), py::arg("max_span") = 0);
+    m.def("gen_uniform_words", &gen_uniform_words, py::arg("n"), py::arg("count"), py::arg("seed") = 2024);
     m.def("gen_random_circuit", &gen_random_circuit, py::arg("n"), py::arg("m"), py::arg("seed"),
           py::arg("max_arity") = 2, py::arg("payloads") = true);
     m.def("random_state", [](int n, std::uint64_t seed) { return to_numpy(random_state(n, seed).amps); });

@@ -9,7 +9,9 @@ product must reproduce:
   hierarchical / adhoc, flat(p) and two_level shapes) and the paper fixtures;
 * EVC plans  (evc_scheduler.cpp): sha256 of plan_to_json, QR and baseline counts;
 * generators (models.cpp): exact payload / coefficient / state bits;
-* dist-sim   (dist_sim.cpp): small QSU output states, expectations, energies.
+* dist-sim   (dist_sim.cpp): small QSU output states, expectations, energies;
+* configs    the BASELINE configs: C1 energies and QR totals (20q, 4 PEs, lazy
+  and eager), C4 HEA schedules, C5 uniform-word plans (Rng(2024)).
 
     python tests/golden/make_golden.py        # needs oracle/_ref (make -C oracle ref)
 """
@@ -151,13 +153,85 @@ def distsim():
     return out
 
 
+def hea_arrays(n, depth):
+    """Targets of gen_hea: per layer RY on every qubit, RZ on
+    every qubit, CZ(q, q+1) for even q, then odd q.  Payload-free: only the
+    targets matter to the schedulers."""
+    ar, tg = [], []
+    for _ in range(depth):
+        for _ in range(2):
+            for q in range(n):
+                ar.append(1)
+                tg.append(q)
+        for parity in (0, 1):
+            for q in range(parity, n - 1, 2):
+                ar.append(2)
+                tg += [q, q + 1]
+    return np.array(ar, dtype=np.int32), np.array(tg, dtype=np.int32)
+
+
+def hea_circuit(n, depth):
+    import ctypes as C
+    ar, tg = hea_arrays(n, depth)
+    return R.Circuit(R.lib().ref_circuit_from_arrays(n, len(ar), ar.ctypes.data_as(C.POINTER(C.c_int)),
+                                                     tg.ctypes.data_as(C.POINTER(C.c_int)), None))
+
+
+def configs():
+    """The BASELINE.json configs as the reference computes them:
+    C1 energies + QR totals, C4 HEA schedules, C5 uniform-word plans."""
+    out = {}
+    # C1: 20q GateFabric layers 80 seed 1, full JW seed 1, flat(4), lazy vs eager
+    circ = R.Circuit.gatefabric(20, 80, 1, True)
+    terms = R.Terms.jw(20, 1, 0)
+    for sched in ("flat", "adhoc"):
+        e, a, b = R.evaluate_energy(circ, terms, sched, 4, 0, 0, True, 4)
+        out[f"c1_{sched}"] = {"energy": e, "energy_hex": float(e).hex(), "qsu_qr": a, "evc_qr": b}
+    # C4: HEA depth 20 schedules at 30/32/34 qubits
+    hea = []
+    for n in (20, 30, 32, 34):
+        c = hea_circuit(n, 20)
+        for p in (2, 4, 8):
+            for sched in ("flat", "adhoc"):
+                d = c.schedule(sched, p, 0, 0)
+                hea.append({"circuit": f"hea:{n}:20", "shape": f"flat{p}", "scheduler": sched,
+                            "counts": d["counts"], "tiles": len(d["schedule"]["tiles"]),
+                            "sha": sha(d["schedule"]),
+                            "events_sha": sha([e["after_pos_of"] for e in d["events"]])})
+    out["hea_schedules"] = hea
+    # C5 stress: 10,000 uniform words, Rng(2024)
+    uni = []
+    for n, count, p in ((34, 10000, 8), (34, 10000, 4), (34, 10000, 2), (32, 10000, 4), (30, 1000, 1), (30, 1000, 2)):
+        t = R.Terms.uniform(n, count, 2024)
+        letters, co = t.export()
+        d = t.plan(n, p, 0, 0, True, 8)
+        uni.append({"terms": f"uniform:{n}:{count}:2024", "shape": f"flat{p}", "diag": True,
+                    "words_sha": hashlib.sha256("".join(letters).encode()).hexdigest(),
+                    "coeff_sha": hashlib.sha256(co.tobytes()).hexdigest(),
+                    "qr": d["qr_count"], "groups": d["n_groups"], "tiles": len(d["plan"]["tiles"]),
+                    "sha": sha(d["plan"])})
+    out["uniform_plans"] = uni
+    # small-n uniform-word energies through the reference expectation (GPU parity)
+    for n, count, p in ((16, 200, 1), (16, 200, 4), (18, 300, 2)):
+        psi = R.random_state(n, 500 + n)
+        e, nq, _ = R.expectation(psi, R.Terms.uniform(n, count, 2024), p, 0, 0, True, 4)
+        out[f"evc_uniform_{n}_{count}_rs{500 + n}_p{p}"] = {"energy": [e.real, e.imag], "qr": nq}
+    return out
+
+
 def main():
+    if not R.available():
+        sys.exit("oracle/_ref/libqrtile_ref.so missing: run `make -C oracle ref` first")
+    if sys.argv[1:] == ["configs"]:
+        (HERE / "configs.json").write_text(json.dumps(configs(), indent=0))
+        return
     if not R.available():
         sys.exit("oracle/_ref/libqrtile_ref.so missing: run `make -C oracle ref` first")
     (HERE / "schedules.json").write_text(json.dumps(schedules(), indent=0))
     (HERE / "plans.json").write_text(json.dumps(plans(), indent=0))
     (HERE / "generators.json").write_text(json.dumps(generators(), indent=0))
     (HERE / "distsim.json").write_text(json.dumps(distsim(), indent=0))
+    (HERE / "configs.json").write_text(json.dumps(configs(), indent=0))
     print("golden fixtures written to", HERE)
 
 

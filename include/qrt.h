@@ -64,7 +64,14 @@ qrt_status qrt_comm_init(int rank, int world, int device, const unsigned char id
 qrt_status qrt_comm_barrier(qrt_comm* comm);
 qrt_status qrt_comm_destroy(qrt_comm* comm);
 
-/* ------------------------------------------------------------------- state */
+/* ------------------------------------------------------------------- state
+ * Collective calls.  With a communicator, qrt_state_create, qrt_reorder and
+ * qrt_release_cache are collective.  qrt_reorder may only *record* the QR
+ * (fused into the next gate pass); while one is pending, the next
+ * qrt_apply_gates, qrt_state_upload, qrt_state_download, qrt_norm and
+ * qrt_pauli_expectation execute it first and are then collective as well,
+ * and qrt_pauli_expectation / qrt_norm always are (they gather per-PE
+ * partials).  Every rank must make the same sequence of these calls. */
 /* init_state (dist_sim.cpp:122-131): zero state |0...0> on p PEs.  comm may
  * be NULL (single process, all p PEs on `device`); otherwise p must be a
  * multiple of the world size and rank r owns PEs [r*p/w, (r+1)*p/w).
@@ -100,6 +107,24 @@ qrt_status qrt_apply_gates(qrt_state* st, int n_gates, const int* arity, const i
  * change PE over NVLink; collective when comm != NULL.  *relocated receives
  * the number of amplitudes (all PEs) whose owning PE changed. */
 qrt_status qrt_reorder(qrt_state* st, const int* dest, uint64_t* relocated);
+
+/* QR mode of a state: *inplace_qr = 1 when qrt_reorder runs in place (one
+ * buffer per PE: local bit-transposition passes + a pairwise NVLink swap of
+ * slot classes), 0 for the two-buffer push / fused pull
+ * exchange.  Chosen at qrt_state_create: QRT_QR_INPLACE=1/0 forces it, unset
+ * picks in-place when two sub-vectors per PE do not fit in free device
+ * memory (e.g. 34 qubits on 2 GPUs); all ranks agree (collective).
+ * *sm_count = multiprocessors of the state's device (grid sizing). */
+qrt_status qrt_state_mode(const qrt_state* st, int* inplace_qr, int* sm_count);
+
+/* Host-only: the in-place decomposition of a reorder map (no device).
+ * local_pairs0 / local_pairs1 receive n0 / n1 disjoint local position
+ * transpositions (a, c) applied in that order, cross_pairs k (local slot,
+ * PE-index bit) transpositions exchanged between PEs.  Arrays of 2*64 ints.
+ * Fails with QRT_ERR_CONFIG when a global position would move to another
+ * global position. */
+qrt_status qrt_reorder_inplace_plan(int n, int p, const int* dest, int* local_pairs0, int* n0, int* local_pairs1,
+                                    int* n1, int* cross_pairs, int* k);
 
 /* Host-only replay of qrt_reorder's index mapping (no device needed): for
  * each of the 2^(n-g) amplitudes of source PE `src_pe`, the destination PE

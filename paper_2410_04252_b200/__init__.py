@@ -40,6 +40,33 @@ def load_libqrt() -> ctypes.CDLL:
     return ctypes.CDLL(libqrt_path())
 
 
+def inplace_reorder_plan(n: int, p: int, dest) -> tuple[list, list, list]:
+    """The in-place decomposition libqrt uses for qrt_reorder(dest) on a
+    single-buffer state (qrt_reorder_inplace_plan): two passes of disjoint
+    local position transpositions, then the (local slot, PE bit) pairs that
+    are swapped between PEs.  Host only."""
+    lib = load_libqrt()
+    a0, a1, cr = (ctypes.c_int * 128)(), (ctypes.c_int * 128)(), (ctypes.c_int * 128)()
+    n0, n1, k = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    rc = lib.qrt_reorder_inplace_plan(n, p, (ctypes.c_int * n)(*dest), a0, ctypes.byref(n0), a1, ctypes.byref(n1),
+                                      cr, ctypes.byref(k))
+    if rc != 0:
+        lib.qrt_last_error.restype = ctypes.c_char_p
+        raise Error(lib.qrt_last_error().decode())
+    pairs = lambda arr, c: [(arr[2 * i], arr[2 * i + 1]) for i in range(c.value)]  # noqa: E731
+    return pairs(a0, n0), pairs(a1, n1), pairs(cr, k)
+
+
+def state_mode(state) -> dict:
+    """QR mode of a live state: {"inplace_qr": bool, "sm_count": int}."""
+    lib = load_libqrt()
+    ip, sm = ctypes.c_int(), ctypes.c_int()
+    rc = lib.qrt_state_mode(ctypes.c_void_p(state.handle()), ctypes.byref(ip), ctypes.byref(sm))
+    if rc != 0:
+        raise Error("qrt_state_mode failed")
+    return {"inplace_qr": bool(ip.value), "sm_count": sm.value}
+
+
 def init_distributed(device: int | None = None):
     """One process per GPU: read RANK/WORLD_SIZE/LOCAL_RANK, share the NCCL id
     over torch.distributed (gloo, plumbing only) and create the libqrt

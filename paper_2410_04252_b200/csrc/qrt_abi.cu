@@ -101,6 +101,18 @@ __global__ void zero_state_kernel(amp_t* __restrict__ v, std::uint64_t count, in
 // parks and reuses in the same order, so peer mappings stay valid.
 std::mutex g_cache_mu;
 std::vector<qrt_state*> g_cache;
+// Communicators alive now, by generation id: a parked state is reused only by
+// the communicator that created it (a new one allocated at the same address
+// has a new id), and a state whose communicator is gone is freed, not parked.
+std::uint64_t g_comm_gen = 0;
+std::vector<std::pair<const qrt_comm*, std::uint64_t>> g_live_comms;
+
+bool comm_alive(const qrt_comm* c, std::uint64_t gen) {
+    if (!c) return true;
+    for (auto& [p, g] : g_live_comms)
+        if (p == c && g == gen) return true;
+    return false;
+}
 
 void free_state(qrt_state* st) {
     DeviceGuard g(st->device);
@@ -119,11 +131,13 @@ void free_state(qrt_state* st) {
     delete st;
 }
 
-qrt_state* take_cached(int n, int p, int device, qrt_comm* comm) {
+qrt_state* take_cached(int n, int p, int device, qrt_comm* comm, int inplace) {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     for (std::size_t i = 0; i < g_cache.size(); ++i) {
         qrt_state* st = g_cache[i];
-        if (st->n == n && st->p == p && st->device == device && st->comm == comm) {
+        if (st->n == n && st->p == p && st->device == device && st->comm == comm &&
+            (inplace < 0 || st->inplace == (inplace != 0)) &&
+            (!comm || st->comm_gen == comm->gen)) {
             g_cache.erase(g_cache.begin() + static_cast<std::ptrdiff_t>(i));
             return st;
         }
@@ -131,11 +145,33 @@ qrt_state* take_cached(int n, int p, int device, qrt_comm* comm) {
     return nullptr;
 }
 
-int grid_for(std::uint64_t items, int threads) {
-    int sms = 148;
+int grid_for(std::uint64_t items, int threads, int sms) {
     std::uint64_t want = (items + threads - 1) / threads;
     std::uint64_t cap = static_cast<std::uint64_t>(sms) * 8;
     return static_cast<int>(want < cap ? (want == 0 ? 1 : want) : cap);
+}
+
+// In-place QR policy (QRT_QR_INPLACE: 0 never, 1 always, unset = auto):
+// auto picks it when this process's sub-vectors twice over would not fit in
+// the device memory free now (minus 4 GiB of headroom), e.g. 34 qubits on 2
+// GPUs (2 x 128 GiB per GPU).
+int forced_inplace(int p) {  // -1: automatic
+    if (p < 2) return 0;
+    const char* e = std::getenv("QRT_QR_INPLACE");
+    if (e && *e) return std::atoi(e) != 0 ? 1 : 0;
+    return -1;
+}
+
+bool choose_inplace(int p, std::uint64_t state_bytes) {
+    const int f = forced_inplace(p);
+    if (f >= 0) return f != 0;
+    std::size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    const std::uint64_t headroom = 4ull << 30;
+    return 2 * state_bytes + headroom > free_b;
 }
 
 }  // namespace
@@ -158,13 +194,14 @@ void nccl_check(ncclResult_t r, const char* what, const char* file, int line) {
 ProfileScope::ProfileScope(qrt_state* s, int f) : st(s), fam(f) {
     if (st->profile) QRT_CUDA(cudaEventRecord(st->ev0, st->stream));
 }
-ProfileScope::~ProfileScope() noexcept(false) {
+ProfileScope::~ProfileScope() {
     if (!st->profile) return;
-    QRT_CUDA(cudaEventRecord(st->ev1, st->stream));
-    QRT_CUDA(cudaEventSynchronize(st->ev1));
+    // Destructors must not throw (this one may run during unwinding): a
+    // failure here leaves the timing out and is caught by the next checked call.
     float ms = 0.f;
-    QRT_CUDA(cudaEventElapsedTime(&ms, st->ev0, st->ev1));
-    st->stats[fam].ms += ms;
+    if (cudaEventRecord(st->ev1, st->stream) == cudaSuccess && cudaEventSynchronize(st->ev1) == cudaSuccess &&
+        cudaEventElapsedTime(&ms, st->ev0, st->ev1) == cudaSuccess)
+        st->stats[fam].ms += ms;
 }
 
 void ensure_alt(qrt_state* st) {
@@ -212,6 +249,7 @@ double* ensure_red(qrt_state* st, std::size_t doubles) {
 void barrier_on_stream(qrt_state* st) {
     if (!st->comm || st->comm->world == 1) return;
     QRT_NCCL(ncclAllReduce(st->d_flag, st->d_flag, 1, ncclInt32, ncclSum, st->comm->nccl, st->stream));
+    st->spare_busy = false;  // work enqueued before this point is complete on every rank
 }
 
 }  // namespace qrt
@@ -264,6 +302,13 @@ qrt_status qrt_comm_init(int rank, int world, int device, const unsigned char id
             ncclUniqueId uid;
             std::memcpy(&uid, id, 128);
             QRT_NCCL(ncclCommInitRank(&c->nccl, world, uid, rank));
+            QRT_CUDA(cudaMalloc(&c->d_flag, sizeof(int)));
+            QRT_CUDA(cudaMemset(c->d_flag, 0, sizeof(int)));
+        }
+        {
+            std::lock_guard<std::mutex> lk(g_cache_mu);
+            c->gen = ++g_comm_gen;
+            g_live_comms.emplace_back(c, c->gen);
         }
         *out = c;
     });
@@ -274,17 +319,44 @@ qrt_status qrt_comm_barrier(qrt_comm* comm) {
         require(comm != nullptr, QRT_ERR_INVALID, "null comm");
         if (comm->world == 1) return;
         DeviceGuard g(comm->device);
-        int* d = nullptr;
-        QRT_CUDA(cudaMalloc(&d, sizeof(int)));
-        QRT_NCCL(ncclAllReduce(d, d, 1, ncclInt32, ncclSum, comm->nccl, nullptr));
+        QRT_NCCL(ncclAllReduce(comm->d_flag, comm->d_flag, 1, ncclInt32, ncclSum, comm->nccl, nullptr));
         QRT_CUDA(cudaStreamSynchronize(nullptr));
-        QRT_CUDA(cudaFree(d));
     });
 }
 
 qrt_status qrt_comm_destroy(qrt_comm* comm) {
     return guarded([&] {
         if (!comm) return;
+        // Parked states of this communicator: every rank parks in the same
+        // order, so meet once (no peer still reads an IPC-exported buffer),
+        // then free them.
+        std::vector<qrt_state*> mine;
+        {
+            std::lock_guard<std::mutex> lk(g_cache_mu);
+            for (auto it = g_cache.begin(); it != g_cache.end();) {
+                if ((*it)->comm == comm && (*it)->comm_gen == comm->gen) {
+                    mine.push_back(*it);
+                    it = g_cache.erase(it);
+                } else {
+                    ++it;
+                }
+            }
+            for (auto it = g_live_comms.begin(); it != g_live_comms.end(); ++it)
+                if (it->first == comm && it->second == comm->gen) {
+                    g_live_comms.erase(it);
+                    break;
+                }
+        }
+        if (!mine.empty() && comm->world > 1) {
+            DeviceGuard g(comm->device);
+            QRT_NCCL(ncclAllReduce(comm->d_flag, comm->d_flag, 1, ncclInt32, ncclSum, comm->nccl, nullptr));
+            QRT_CUDA(cudaStreamSynchronize(nullptr));
+        }
+        for (qrt_state* st : mine) free_state(st);
+        if (comm->d_flag) {
+            DeviceGuard g(comm->device);
+            cudaFree(comm->d_flag);
+        }
         if (comm->nccl) ncclCommDestroy(comm->nccl);
         delete comm;
     });
@@ -309,12 +381,20 @@ qrt_status qrt_state_create(int n, int p, int device, qrt_comm* comm, qrt_state*
         }
         require(device >= 0 && device < ndev, QRT_ERR_NO_DEVICE, "device index out of range");
         DeviceGuard dg(device);
-        if (qrt_state* cached = take_cached(n, p, device, comm)) {
+        // FusedSource / QrArgs / XchgArgs address every PE of a multi-process
+        // state through fixed 64-entry tables.
+        require(world == 1 || p <= kMaxLocalPEs, QRT_ERR_CONFIG,
+                "p = " + std::to_string(p) + " exceeds the 64-PE limit of a multi-process state");
+        const std::uint64_t state_bytes = (1ull << (n - g)) * sizeof(amp_t) * static_cast<std::uint64_t>(p / world);
+        // a parked state of the same shape is reused whatever its QR mode
+        // (unless QRT_QR_INPLACE forces one): its memory is what the
+        // automatic choice would otherwise miss
+        if (qrt_state* cached = take_cached(n, p, device, comm, forced_inplace(p))) {
             // buffer parity is kept (peers address the same physical buffers)
             cached->profile = false;
             for (auto& sct : cached->stats) sct = qrt_kernel_stats{};
             for (int i = 0; i < cached->pe_count; ++i)
-                zero_state_kernel<<<grid_for(cached->amps, 256), 256, 0, cached->stream>>>(
+                zero_state_kernel<<<grid_for(cached->amps, 256, cached->sm_count), 256, 0, cached->stream>>>(
                     cached->live(i), cached->amps, cached->pe_begin + i == 0);
             QRT_CUDA(cudaGetLastError());
             cached->stats[QRT_K_MISC].launches += static_cast<std::uint64_t>(cached->pe_count);
@@ -324,12 +404,16 @@ qrt_status qrt_state_create(int n, int p, int device, qrt_comm* comm, qrt_state*
             return;
         }
 
+        const bool inplace = choose_inplace(p, state_bytes);
         auto st = new qrt_state;
         st->n = n;
         st->p = p;
         st->nl = n - g;
         st->device = device;
         st->comm = comm;
+        st->comm_gen = comm ? comm->gen : 0;
+        st->inplace = inplace;
+        QRT_CUDA(cudaDeviceGetAttribute(&st->sm_count, cudaDevAttrMultiProcessorCount, device));
         st->pe_count = p / world;
         require(st->pe_count <= kMaxLocalPEs, QRT_ERR_CONFIG, "too many PEs per process");
         st->pe_begin = rank * st->pe_count;
@@ -340,12 +424,22 @@ qrt_status qrt_state_create(int n, int p, int device, qrt_comm* comm, qrt_state*
             QRT_CUDA(cudaEventCreate(&st->ev1));
             QRT_CUDA(cudaMalloc(&st->d_flag, sizeof(int)));
             QRT_CUDA(cudaMemsetAsync(st->d_flag, 0, sizeof(int), st->stream));
+            if (comm && world > 1) {  // every rank must take the same QR mode
+                int v = st->inplace ? 1 : 0;
+                QRT_CUDA(cudaMemcpyAsync(st->d_flag, &v, sizeof(int), cudaMemcpyHostToDevice, st->stream));
+                QRT_NCCL(ncclAllReduce(st->d_flag, st->d_flag, 1, ncclInt32, ncclMax, comm->nccl, st->stream));
+                QRT_CUDA(cudaMemcpyAsync(&v, st->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st->stream));
+                QRT_CUDA(cudaStreamSynchronize(st->stream));
+                st->inplace = v != 0;
+            }
             for (int b = 0; b < 2; ++b) {
                 st->bufs[b].assign(static_cast<std::size_t>(st->pe_count), nullptr);
                 st->peer[b].assign(static_cast<std::size_t>(p), nullptr);
             }
             const bool multi = comm && world > 1;
-            const int nb = multi ? 2 : 1;
+            // multi-process: both buffers up front (IPC-exported); in-place
+            // QR states never allocate the second one
+            const int nb = (multi && !st->inplace) ? 2 : 1;
             for (int b = 0; b < nb; ++b)
                 for (int i = 0; i < st->pe_count; ++i)
                     QRT_CUDA(cudaMalloc(&st->bufs[b][static_cast<std::size_t>(i)], st->amps * sizeof(amp_t)));
@@ -353,10 +447,10 @@ qrt_status qrt_state_create(int n, int p, int device, qrt_comm* comm, qrt_state*
                 for (int i = 0; i < st->pe_count; ++i)
                     st->peer[b][static_cast<std::size_t>(st->pe_begin + i)] = st->bufs[b][static_cast<std::size_t>(i)];
             if (multi) {
-                // Exchange IPC handles of both buffers of every PE (all-gather).
-                const std::size_t per = static_cast<std::size_t>(2 * st->pe_count) * sizeof(cudaIpcMemHandle_t);
-                std::vector<cudaIpcMemHandle_t> mine(static_cast<std::size_t>(2 * st->pe_count));
-                for (int b = 0; b < 2; ++b)
+                // Exchange IPC handles of the buffers of every PE (all-gather).
+                const std::size_t per = static_cast<std::size_t>(nb * st->pe_count) * sizeof(cudaIpcMemHandle_t);
+                std::vector<cudaIpcMemHandle_t> mine(static_cast<std::size_t>(nb * st->pe_count));
+                for (int b = 0; b < nb; ++b)
                     for (int i = 0; i < st->pe_count; ++i)
                         QRT_CUDA(cudaIpcGetMemHandle(&mine[static_cast<std::size_t>(b * st->pe_count + i)],
                                                      st->bufs[b][static_cast<std::size_t>(i)]));
@@ -366,18 +460,18 @@ qrt_status qrt_state_create(int n, int p, int device, qrt_comm* comm, qrt_state*
                                          cudaMemcpyHostToDevice, st->stream));
                 QRT_NCCL(ncclAllGather(d_all + per * static_cast<std::size_t>(rank), d_all, per, ncclChar,
                                        comm->nccl, st->stream));
-                std::vector<cudaIpcMemHandle_t> all(static_cast<std::size_t>(2 * st->pe_count * world));
+                std::vector<cudaIpcMemHandle_t> all(static_cast<std::size_t>(nb * st->pe_count * world));
                 QRT_CUDA(cudaMemcpyAsync(all.data(), d_all, per * static_cast<std::size_t>(world), cudaMemcpyDeviceToHost,
                                          st->stream));
                 QRT_CUDA(cudaStreamSynchronize(st->stream));
                 QRT_CUDA(cudaFree(d_all));
                 for (int r = 0; r < world; ++r) {
                     if (r == rank) continue;
-                    for (int b = 0; b < 2; ++b)
+                    for (int b = 0; b < nb; ++b)
                         for (int i = 0; i < st->pe_count; ++i) {
                             void* ptr = nullptr;
                             QRT_CUDA(cudaIpcOpenMemHandle(
-                                &ptr, all[static_cast<std::size_t>((r * 2 + b) * st->pe_count + i)],
+                                &ptr, all[static_cast<std::size_t>((r * nb + b) * st->pe_count + i)],
                                 cudaIpcMemLazyEnablePeerAccess));
                             st->peer[b][static_cast<std::size_t>(r * st->pe_count + i)] = static_cast<amp_t*>(ptr);
                             st->ipc_opened.push_back(ptr);
@@ -385,7 +479,7 @@ qrt_status qrt_state_create(int n, int p, int device, qrt_comm* comm, qrt_state*
                 }
             }
             for (int i = 0; i < st->pe_count; ++i)
-                zero_state_kernel<<<grid_for(st->amps, 256), 256, 0, st->stream>>>(
+                zero_state_kernel<<<grid_for(st->amps, 256, st->sm_count), 256, 0, st->stream>>>(
                     st->bufs[0][static_cast<std::size_t>(i)], st->amps, st->pe_begin + i == 0);
             QRT_CUDA(cudaGetLastError());
             st->stats[QRT_K_MISC].launches += static_cast<std::uint64_t>(st->pe_count);
@@ -412,7 +506,11 @@ qrt_status qrt_state_destroy(qrt_state* st) {
             QRT_CUDA(cudaStreamSynchronize(st->stream));
         }
         std::lock_guard<std::mutex> lk(g_cache_mu);
-        g_cache.push_back(st);  // parked; qrt_release_cache frees
+        if (!comm_alive(st->comm, st->comm_gen)) {
+            free_state(st);  // its communicator is gone: never reusable
+            return;
+        }
+        g_cache.push_back(st);  // parked; qrt_release_cache / qrt_comm_destroy free
     });
 }
 
@@ -423,7 +521,23 @@ qrt_status qrt_release_cache(void) {
             std::lock_guard<std::mutex> lk(g_cache_mu);
             all.swap(g_cache);
         }
+        // Multi-process states: meet first so no peer still reads a buffer
+        // this rank exported (every rank releases the same parked states).
+        for (qrt_state* st : all)
+            if (st->comm && st->comm->world > 1 && comm_alive(st->comm, st->comm_gen)) {
+                DeviceGuard g(st->device);
+                barrier_on_stream(st);
+                QRT_CUDA(cudaStreamSynchronize(st->stream));
+            }
         for (qrt_state* st : all) free_state(st);
+    });
+}
+
+qrt_status qrt_state_mode(const qrt_state* st, int* inplace_qr, int* sm_count) {
+    return guarded([&] {
+        require(st != nullptr, QRT_ERR_INVALID, "null state");
+        if (inplace_qr) *inplace_qr = st->inplace ? 1 : 0;
+        if (sm_count) *sm_count = st->sm_count;
     });
 }
 
@@ -443,7 +557,7 @@ qrt_status qrt_state_set_zero(qrt_state* st) {
         DeviceGuard g(st->device);
         st->qr_pending = false;  // |0...0> is the same in every layout
         for (int i = 0; i < st->pe_count; ++i)
-            zero_state_kernel<<<grid_for(st->amps, 256), 256, 0, st->stream>>>(st->live(i), st->amps,
+            zero_state_kernel<<<grid_for(st->amps, 256, st->sm_count), 256, 0, st->stream>>>(st->live(i), st->amps,
                                                                                st->pe_begin + i == 0);
         QRT_CUDA(cudaGetLastError());
         st->stats[QRT_K_MISC].launches += static_cast<std::uint64_t>(st->pe_count);
@@ -501,6 +615,15 @@ qrt_status qrt_reorder(qrt_state* st, const int* dest, std::uint64_t* relocated)
         std::uint64_t moved = reorder(st, dest);
         QRT_CUDA(cudaStreamSynchronize(st->stream));
         if (relocated) *relocated = moved;
+    });
+}
+
+qrt_status qrt_reorder_inplace_plan(int n, int p, const int* dest, int* local_pairs0, int* n0, int* local_pairs1,
+                                    int* n1, int* cross_pairs, int* k) {
+    return guarded([&] {
+        require(dest && local_pairs0 && n0 && local_pairs1 && n1 && cross_pairs && k, QRT_ERR_INVALID, "null argument");
+        require(n >= 1 && n <= 62, QRT_ERR_CONFIG, "qubit count out of range");
+        reorder_inplace_plan(n, p, dest, local_pairs0, n0, local_pairs1, n1, cross_pairs, k);
     });
 }
 

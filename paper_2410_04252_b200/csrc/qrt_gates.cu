@@ -1596,6 +1596,7 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
             if (fused) {
                 st->cur ^= 1;
                 st->qr_pending = false;
+                st->spare_busy = st->comm && st->comm->world > 1;
             }
             st->stats[QRT_K_GATES].launches++;
             st->stats[QRT_K_GATES].bytes += 32.0 * amps_all;
@@ -1603,12 +1604,16 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
         }
         if (h.T < 0) {  // wide, out of place into the alternate buffer, then copied back
             ensure_alt(st);
+            if (st->spare_busy) {  // peers may still pull our old live buffer (now the spare)
+                barrier_on_stream(st);
+                st->spare_busy = false;
+            }
             const GateOp& g = dev_ops[static_cast<std::size_t>(h.op_begin)];
             const int widx = -h.T - 1;
             for (int i = 0; i < st->pe_count; ++i) {
                 amp_t* src = st->bufs[st->cur][static_cast<std::size_t>(i)];
                 amp_t* dst = st->bufs[st->cur ^ 1][static_cast<std::size_t>(i)];
-                wide_gate_kernel<<<148 * 8, 256, 0, st->stream>>>(src, dst, st->amps, d_pool + g.gmat, g.k,
+                wide_gate_kernel<<<st->sm_count * 8, 256, 0, st->stream>>>(src, dst, st->amps, d_pool + g.gmat, g.k,
                                                                   g.kind == kDiag, d_wpos + widx);
                 QRT_CUDA(cudaGetLastError());
                 QRT_CUDA(cudaMemcpyAsync(src, dst, st->amps * sizeof(amp_t), cudaMemcpyDeviceToDevice, st->stream));
@@ -1634,6 +1639,7 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
         if (fused) {
             st->cur ^= 1;
             st->qr_pending = false;
+            st->spare_busy = st->comm && st->comm->world > 1;
         }
         st->stats[QRT_K_GATES].launches++;
         st->stats[QRT_K_GATES].bytes += 32.0 * amps_all;

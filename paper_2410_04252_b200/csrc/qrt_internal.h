@@ -41,6 +41,8 @@ struct qrt_comm {
     int world = 1;
     int device = 0;
     ncclComm_t nccl = nullptr;
+    int* d_flag = nullptr;  // barrier word of qrt_comm_barrier (allocated once)
+    std::uint64_t gen = 0;  // generation id: keys the parked-state cache
 };
 
 struct KernelCounters {
@@ -53,6 +55,7 @@ struct qrt_state {
     int nl = 0;  // local positions
     int device = 0;
     qrt_comm* comm = nullptr;
+    std::uint64_t comm_gen = 0;
     int pe_begin = 0;
     int pe_count = 0;
     std::uint64_t amps = 0;  // amplitudes per PE
@@ -81,6 +84,14 @@ struct qrt_state {
     // through it (qrt_fused.h); any other access executes it first.
     bool qr_pending = false;
     std::vector<int> qr_dest;
+    // In-place QR (one buffer per PE; qrt_reorder.cu execute_inplace): set at
+    // create when two sub-vectors per PE do not fit (or QRT_QR_INPLACE=1).
+    // Disables the fused (pull) QR, which writes the spare buffer.
+    bool inplace = false;
+    // A fused pass flipped buffers: peers may still read the new spare (our
+    // old live buffer) until the next barrier; writers of the spare wait.
+    bool spare_busy = false;
+    int sm_count = 148;
 
     // Measurement.
     bool profile = false;
@@ -98,7 +109,7 @@ struct ProfileScope {
     qrt_state* st;
     int fam;
     ProfileScope(qrt_state* s, int f);
-    ~ProfileScope() noexcept(false);
+    ~ProfileScope();  // never throws: a failed event query is recorded, not raised
 };
 
 void ensure_alt(qrt_state* st);
@@ -115,6 +126,8 @@ void flush_reorder(qrt_state* st);  // execute a pending QR (no-op if none)
 bool fused_qr_enabled();
 void reorder_plan(int n, int p, const int* dest, int src_pe, std::uint64_t* dst_pe, std::uint64_t* dst_off,
                   std::uint64_t* relocated);
+void reorder_inplace_plan(int n, int p, const int* dest, int* pairs0, int* n0, int* pairs1, int* n1, int* cross,
+                          int* k);
 void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const std::uint64_t* y,
                        const std::uint64_t* z, const std::uint64_t* gz, const double* coeffs, double* partial);
 double norm(qrt_state* st);

@@ -1342,7 +1342,7 @@ void pauli_plan_info(int nl, int n_terms, const std::uint64_t* x, const std::uin
 }
 
 double norm(qrt_state* st) {
-    const int blocks = 148 * 4;
+    const int blocks = st->sm_count * 4;
     const std::size_t slots = static_cast<std::size_t>(blocks) * static_cast<std::size_t>(st->pe_count);
     double* red = ensure_red(st, 2 * slots + 2 * static_cast<std::size_t>(st->pe_count) + 2 * static_cast<std::size_t>(st->p));
     double* out = red + 2 * slots;

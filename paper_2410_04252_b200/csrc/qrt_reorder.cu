@@ -177,7 +177,296 @@ std::uint64_t build_map(int n, int nl, int pe_begin, const int* dest, QrMap& a, 
     return relocated;
 }
 
+// ---------------------------------------------------------------------------
+// In-place QR (SURVEY.md §7 "in-place QR mandatory" at 34 qubits / p = 2,
+// where two 128 GiB sub-vectors per GPU do not fit in 180 GB).  The reference
+// builds a full second copy (dist_sim.cpp:224-233); here the position
+// permutation `dest` is split into
+//   rho   a permutation of local positions (staying qubits that move, and
+//         the departing qubit's move to the slot its arriving partner takes),
+//         applied as at most two involutions = passes of disjoint local
+//         bit-transpositions (a 2-cycle is one pass), and
+//   cross k transpositions (local slot d_i <-> PE bit b_i): a pairwise
+//         symmetric exchange — PE j's slot class s swaps with PE s's slot
+//         class j at the same offsets otherwise.
+// Every element pair is read and written by exactly one thread (the pair's
+// two PEs split the classes on one free position f), so both passes run in
+// place with no staging buffer at all: the exchange reads the partner's
+// amplitude over NVLink and stores this PE's amplitude into the partner's
+// slot, so each direction of the link carries the same bytes as the push
+// exchange, and the 2^-k of the data that stays is never touched.
+
+struct Deposit {
+    int E = 0;                      // low enumeration bits (table lookup)
+    int n_hi = 0;                   // enumeration bits above E
+    int hi_pos[64] = {};
+    std::uint64_t tab[2][32] = {};  // e (two 5-bit halves) -> offset bits
+};
+
+void make_deposit(const std::vector<int>& rest, Deposit& d) {
+    d = Deposit{};
+    d.E = std::min(10, static_cast<int>(rest.size()));
+    d.n_hi = static_cast<int>(rest.size()) - d.E;
+    for (int h = 0; h < 2; ++h)
+        for (int e = 0; e < 32; ++e) {
+            std::uint64_t v = 0;
+            for (int b = 0; b < 5; ++b) {
+                const int bit = h * 5 + b;
+                if (bit < d.E && ((e >> b) & 1)) v |= 1ull << rest[static_cast<std::size_t>(bit)];
+            }
+            d.tab[h][e] = v;
+        }
+    for (int i = 0; i < d.n_hi; ++i) d.hi_pos[i] = rest[static_cast<std::size_t>(d.E + i)];
+}
+
+__device__ __forceinline__ std::uint64_t dep_hi(const Deposit& d, std::uint64_t chunk) {
+    std::uint64_t v = 0;
+    for (int i = 0; i < d.n_hi; ++i) v |= ((chunk >> i) & 1ull) << d.hi_pos[i];
+    return v;
+}
+__device__ __forceinline__ std::uint64_t dep_lo(const Deposit& d, int e) {
+    return d.tab[0][e & 31] | d.tab[1][(e >> 5) & 31];
+}
+
+struct XchgArgs {
+    amp_t* pe_ptr[kMaxLocalPEs];  // live buffer of every PE (IPC peer table)
+    int pe_begin;
+    int k;
+    int d_pos[8];   // local slot of transposition i
+    int pe_bit[8];  // PE-index bit of transposition i
+    int f;          // free local position splitting each class pair between its two PEs (-1: none)
+    Deposit dep;    // the remaining local positions
+};
+
+constexpr int kXchgUnroll = 4;
+
+__global__ void __launch_bounds__(256) exchange_kernel(const __grid_constant__ XchgArgs a) {
+    const int j = a.pe_begin + static_cast<int>(blockIdx.y);
+    int jc = 0;
+    for (int i = 0; i < a.k; ++i) jc |= ((j >> a.pe_bit[i]) & 1) << i;
+    const std::uint64_t chunks = 1ull << a.dep.n_hi;
+    const std::uint64_t work = static_cast<std::uint64_t>((1 << a.k) - 1) * chunks;
+    const int E = 1 << a.dep.E;
+    amp_t* __restrict__ mine = a.pe_ptr[j];
+    for (std::uint64_t w = blockIdx.x; w < work; w += gridDim.x) {
+        const int ci = static_cast<int>(w / chunks);
+        const std::uint64_t chunk = w % chunks;
+        const int s = ci >= jc ? ci + 1 : ci;  // the partner's class (never jc: that class stays)
+        int sp = j;
+        std::uint64_t ob = 0, pb = 0;
+        for (int i = 0; i < a.k; ++i) {
+            const int sb = (s >> i) & 1, jb = (jc >> i) & 1;
+            sp = (sp & ~(1 << a.pe_bit[i])) | (sb << a.pe_bit[i]);
+            ob |= static_cast<std::uint64_t>(sb) << a.d_pos[i];
+            pb |= static_cast<std::uint64_t>(jb) << a.d_pos[i];
+        }
+        if (a.f >= 0) {
+            const std::uint64_t hb = j < sp ? 0ull : 1ull;
+            ob |= hb << a.f;
+            pb |= hb << a.f;
+        } else if (j > sp) {
+            continue;  // no free position: the lower PE of the pair does it all
+        }
+        const std::uint64_t hi = dep_hi(a.dep, chunk);
+        ob |= hi;
+        pb |= hi;
+        amp_t* __restrict__ peer = a.pe_ptr[sp];
+        for (int e0 = threadIdx.x; e0 < E; e0 += kXchgUnroll * blockDim.x) {
+            amp_t x[kXchgUnroll], y[kXchgUnroll];
+            std::uint64_t lo[kXchgUnroll];
+#pragma unroll
+            for (int u = 0; u < kXchgUnroll; ++u) {
+                const int e = e0 + u * static_cast<int>(blockDim.x);
+                lo[u] = e < E ? dep_lo(a.dep, e) : 0;
+                if (e < E) {
+                    x[u] = __ldcs(&mine[ob | lo[u]]);
+                    y[u] = __ldcs(&peer[pb | lo[u]]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kXchgUnroll; ++u) {
+                const int e = e0 + u * static_cast<int>(blockDim.x);
+                if (e < E) {
+                    __stcs(&mine[ob | lo[u]], y[u]);
+                    __stcs(&peer[pb | lo[u]], x[u]);
+                }
+            }
+        }
+    }
+    __threadfence_system();  // peer stores visible before the stream-ordered barrier
+}
+
+struct LocalSwapArgs {
+    amp_t* ptr[kMaxLocalPEs];  // this process's live buffers
+    int m;                     // disjoint transpositions (a_i <-> c_i), a_i < c_i
+    int a_pos[8];
+    int c_pos[8];
+    Deposit dep;               // the other local positions
+};
+
+// One involution of local positions, in place: the element with pattern v on
+// the pair bits swaps with the pattern where each pair's two bits are
+// exchanged; the lower offset of the two does the swap (block-uniform test).
+__global__ void __launch_bounds__(256) local_swap_kernel(const __grid_constant__ LocalSwapArgs a) {
+    amp_t* __restrict__ v = a.ptr[blockIdx.y];
+    const std::uint64_t chunks = 1ull << a.dep.n_hi;
+    const std::uint64_t work = (1ull << (2 * a.m)) * chunks;
+    const int E = 1 << a.dep.E;
+    for (std::uint64_t w = blockIdx.x; w < work; w += gridDim.x) {
+        const int pat = static_cast<int>(w / chunks);
+        const std::uint64_t chunk = w % chunks;
+        std::uint64_t ob = 0, pb = 0;
+        for (int i = 0; i < a.m; ++i) {
+            const std::uint64_t ba = (pat >> (2 * i)) & 1, bc = (pat >> (2 * i + 1)) & 1;
+            ob |= (ba << a.a_pos[i]) | (bc << a.c_pos[i]);
+            pb |= (bc << a.a_pos[i]) | (ba << a.c_pos[i]);
+        }
+        if (pb <= ob) continue;  // fixed (equal) or handled from the partner's pattern
+        const std::uint64_t hi = dep_hi(a.dep, chunk);
+        ob |= hi;
+        pb |= hi;
+        for (int e0 = threadIdx.x; e0 < E; e0 += kXchgUnroll * blockDim.x) {
+            amp_t x[kXchgUnroll], y[kXchgUnroll];
+            std::uint64_t lo[kXchgUnroll];
+#pragma unroll
+            for (int u = 0; u < kXchgUnroll; ++u) {
+                const int e = e0 + u * static_cast<int>(blockDim.x);
+                lo[u] = e < E ? dep_lo(a.dep, e) : 0;
+                if (e < E) {
+                    x[u] = __ldcs(&v[ob | lo[u]]);
+                    y[u] = __ldcs(&v[pb | lo[u]]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kXchgUnroll; ++u) {
+                const int e = e0 + u * static_cast<int>(blockDim.x);
+                if (e < E) {
+                    __stcs(&v[ob | lo[u]], y[u]);
+                    __stcs(&v[pb | lo[u]], x[u]);
+                }
+            }
+        }
+    }
+}
+
+// dest (position permutation) -> two passes of local transpositions + the
+// cross transpositions.  Requires every global position to be fed by itself
+// or by a local position (true for every flat / one-box QR event,
+// layout.cpp:96-161); anything else is rejected.
+struct InplacePlan {
+    std::vector<std::pair<int, int>> local[2];
+    std::vector<std::pair<int, int>> cross;  // (local slot, PE bit)
+};
+
+InplacePlan plan_inplace(int n, int nl, const int* dest) {
+    std::vector<int> src_of(static_cast<std::size_t>(n), -1);
+    for (int s = 0; s < n; ++s) src_of[static_cast<std::size_t>(dest[s])] = s;
+    InplacePlan P;
+    std::vector<int> rho(static_cast<std::size_t>(nl), -1);
+    for (int x = 0; x < nl; ++x) {
+        const int t = dest[x];
+        if (t < nl) {
+            rho[static_cast<std::size_t>(x)] = t;  // staying qubit
+        } else {
+            const int d = dest[t];  // the arriving qubit's slot
+            if (d >= nl) fail(QRT_ERR_CONFIG, "in-place reorder: global position moves to another global position");
+            rho[static_cast<std::size_t>(x)] = d;
+            P.cross.emplace_back(d, t - nl);
+        }
+    }
+    for (int t = nl; t < n; ++t) {
+        const int s = src_of[static_cast<std::size_t>(t)];
+        if (s >= nl && s != t) fail(QRT_ERR_CONFIG, "in-place reorder: global position moves to another global position");
+    }
+    // rho = tau2 o tau1 per cycle (x_0 -> x_1 -> ... -> x_{c-1}):
+    // tau1(x_i) = x_{-i}, tau2(x_i) = x_{1-i} (indices mod c).
+    std::vector<char> seen(static_cast<std::size_t>(nl), 0);
+    for (int x0 = 0; x0 < nl; ++x0) {
+        if (seen[static_cast<std::size_t>(x0)]) continue;
+        std::vector<int> cyc;
+        for (int x = x0; !seen[static_cast<std::size_t>(x)]; x = rho[static_cast<std::size_t>(x)]) {
+            seen[static_cast<std::size_t>(x)] = 1;
+            cyc.push_back(x);
+        }
+        const int c = static_cast<int>(cyc.size());
+        if (c < 2) continue;
+        for (int pass = 0; pass < 2; ++pass)
+            for (int i = 0; i < c; ++i) {
+                const int jdx = ((pass == 0 ? -i : 1 - i) % c + c) % c;
+                if (i < jdx) {
+                    const int a = cyc[static_cast<std::size_t>(i)], b = cyc[static_cast<std::size_t>(jdx)];
+                    P.local[pass].emplace_back(std::min(a, b), std::max(a, b));
+                }
+            }
+    }
+    if (P.local[0].empty()) std::swap(P.local[0], P.local[1]);
+    return P;
+}
+
+void launch_local_swaps(qrt_state* st, const std::vector<std::pair<int, int>>& pairs) {
+    for (std::size_t base = 0; base < pairs.size(); base += 8) {
+        LocalSwapArgs a{};
+        a.m = static_cast<int>(std::min<std::size_t>(8, pairs.size() - base));
+        std::vector<char> used(static_cast<std::size_t>(st->nl), 0);
+        for (int i = 0; i < a.m; ++i) {
+            a.a_pos[i] = pairs[base + static_cast<std::size_t>(i)].first;
+            a.c_pos[i] = pairs[base + static_cast<std::size_t>(i)].second;
+            used[static_cast<std::size_t>(a.a_pos[i])] = used[static_cast<std::size_t>(a.c_pos[i])] = 1;
+        }
+        std::vector<int> rest;
+        for (int x = 0; x < st->nl; ++x)
+            if (!used[static_cast<std::size_t>(x)]) rest.push_back(x);
+        make_deposit(rest, a.dep);
+        for (int i = 0; i < st->pe_count; ++i) a.ptr[i] = st->live(i);
+        const std::uint64_t work = (1ull << (2 * a.m)) << a.dep.n_hi;
+        const unsigned gx = static_cast<unsigned>(std::min<std::uint64_t>(work, static_cast<std::uint64_t>(st->sm_count) * 8));
+        local_swap_kernel<<<dim3(gx, static_cast<unsigned>(st->pe_count)), 256, 0, st->stream>>>(a);
+        QRT_CUDA(cudaGetLastError());
+        st->stats[QRT_K_QR].launches++;
+    }
+}
+
+void execute_inplace(qrt_state* st, const int* dest, std::uint64_t relocated) {
+    if (st->p > kMaxLocalPEs) fail(QRT_ERR_CONFIG, "too many PEs for the in-place reorder kernel");
+    const InplacePlan P = plan_inplace(st->n, st->nl, dest);
+    ProfileScope prof(st, QRT_K_QR);
+    for (int pass = 0; pass < 2; ++pass)
+        if (!P.local[pass].empty()) launch_local_swaps(st, P.local[pass]);
+    if (P.cross.empty()) return;
+    if (P.cross.size() > 8) fail(QRT_ERR_CONFIG, "reorder moves more than 8 local bits to global positions");
+    XchgArgs a{};
+    a.pe_begin = st->pe_begin;
+    a.k = static_cast<int>(P.cross.size());
+    std::vector<char> used(static_cast<std::size_t>(st->nl), 0);
+    for (int i = 0; i < a.k; ++i) {
+        a.d_pos[i] = P.cross[static_cast<std::size_t>(i)].first;
+        a.pe_bit[i] = P.cross[static_cast<std::size_t>(i)].second;
+        used[static_cast<std::size_t>(a.d_pos[i])] = 1;
+    }
+    a.f = -1;
+    for (int x = st->nl - 1; x >= 0; --x)
+        if (!used[static_cast<std::size_t>(x)]) {
+            a.f = x;
+            used[static_cast<std::size_t>(x)] = 1;
+            break;
+        }
+    std::vector<int> rest;
+    for (int x = 0; x < st->nl; ++x)
+        if (!used[static_cast<std::size_t>(x)]) rest.push_back(x);
+    make_deposit(rest, a.dep);
+    for (int pe = 0; pe < st->p; ++pe) a.pe_ptr[pe] = st->peer[st->cur][static_cast<std::size_t>(pe)];
+    barrier_on_stream(st);  // every peer is done with the buffers touched here
+    const std::uint64_t work = static_cast<std::uint64_t>((1 << a.k) - 1) << a.dep.n_hi;
+    const unsigned gx = static_cast<unsigned>(std::min<std::uint64_t>(work, static_cast<std::uint64_t>(st->sm_count) * 8));
+    exchange_kernel<<<dim3(gx, static_cast<unsigned>(st->pe_count)), 256, 0, st->stream>>>(a);
+    QRT_CUDA(cudaGetLastError());
+    barrier_on_stream(st);  // every peer's stores into this PE have landed
+    st->stats[QRT_K_QR].launches++;
+    st->stats[QRT_K_QR].bytes += 16.0 * static_cast<double>(relocated) * st->pe_count / st->p;
+}
+
 }  // namespace
+
 
 bool fused_qr_enabled() {
     static const bool on = [] {
@@ -223,6 +512,10 @@ std::uint64_t reorder(qrt_state* st, const int* dest) {
     const std::uint64_t relocated = build_map(st->n, st->nl, st->pe_begin, dest, m, identity);
     if (identity) return 0;
     flush_reorder(st);
+    if (st->inplace) {
+        execute_inplace(st, dest, relocated);
+        return relocated;
+    }
     // Pulling a tile's sources over NVLink scatters each CTA's reads over the
     // whole peer buffer; past 2^30 amplitudes (16 GiB) per PE the translation
     // misses outweigh the saved exchange (34-qubit HEA on 4 GPUs: 0.31 s
@@ -244,6 +537,26 @@ void flush_reorder(qrt_state* st) {
     if (!st->qr_pending) return;
     st->qr_pending = false;
     execute_reorder(st, st->qr_dest.data());
+}
+
+void reorder_inplace_plan(int n, int p, const int* dest, int* pairs0, int* n0, int* pairs1, int* n1, int* cross,
+                          int* k) {
+    if (p < 1 || (p & (p - 1))) fail(QRT_ERR_CONFIG, "p must be a power of two");
+    const int nl = n - __builtin_ctz(static_cast<unsigned>(p));
+    QrMap m{};
+    bool identity = false;
+    (void)build_map(n, nl, 0, dest, m, identity);  // validates the permutation
+    const InplacePlan P = plan_inplace(n, nl, dest);
+    auto put = [](const std::vector<std::pair<int, int>>& v, int* out, int* cnt) {
+        *cnt = static_cast<int>(v.size());
+        for (std::size_t i = 0; i < v.size(); ++i) {
+            out[2 * i] = v[i].first;
+            out[2 * i + 1] = v[i].second;
+        }
+    };
+    put(P.local[0], pairs0, n0);
+    put(P.local[1], pairs1, n1);
+    put(P.cross, cross, k);
 }
 
 // Host-side replay of the kernel's index mapping for one source PE: for every

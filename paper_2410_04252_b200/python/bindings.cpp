@@ -330,7 +330,8 @@ PYBIND11_MODULE(_qrtile, m) {
             qrt_state_stream(s.device->handle, &p);
             return reinterpret_cast<std::uintptr_t>(p);
         })
-        .def("synchronize", [](DistributedState& s) { qrt_synchronize(s.device->handle); });
+        .def("synchronize", [](DistributedState& s) { qrt_synchronize(s.device->handle); })
+        .def("handle", [](const DistributedState& s) { return reinterpret_cast<std::uintptr_t>(s.device->handle); });
 
     m.def("init_state", [](int n, const ClusterShape& shape) { return init_state(n, shape); });
     m.def("init_state_from", [](const CArray& amps, const ClusterShape& shape) {

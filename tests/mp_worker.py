@@ -24,16 +24,31 @@ def main():
     import torch.distributed as dist
 
     results = {}
-    for n, layers, ppr in ((10, 8, 1), (14, 6, 2), (16, 4, 1)):
+    cases = [(10, 8, 1, "0"), (14, 6, 2, "0"), (16, 4, 1, "0"), (14, 6, 2, "1"), (16, 4, 1, "1"), (14, 4, 1, "wide")]
+    for n, layers, ppr, mode in cases:
+        # QRT_QR_INPLACE is read at state creation: "1" = in-place QR (one
+        # buffer per PE, pairwise NVLink swap), "0" = push / fused pull
+        os.environ["QRT_QR_INPLACE"] = "1" if mode == "1" else "0"
         p = world * ppr
         circuit = qb.gen_gatefabric(n, layers, 3, True)
+        if mode == "wide":
+            # an 8-qubit gate between GateFabric layers: after a fused QR the
+            # wide pass writes the spare buffer peers may still be reading
+            ops = list(circuit.operators)
+            half = len(ops) // 2
+            wide = qb.make_gate(half, [7, 0, 3, 1, 6, 2, 5, 4], qb.random_unitary(8, 77))
+            ops = [qb.make_gate(i, list(op.targets), op.payload) for i, op in enumerate(ops[:half])] + [wide] + \
+                  [qb.make_gate(half + 1 + i, list(op.targets), op.payload) for i, op in enumerate(ops[half:])]
+            circuit = qb.Circuit(n, ops)
         deps = qb.build_dependency_graph(circuit)
         shape = qb.ClusterShape.flat(p)
         terms = qb.gen_synthetic_jw(n, 9, 8)
         for name, fn in (("flat", qb.flat_tiling), ("adhoc", qb.adhoc_schedule)):
+            name = f"{name}:{mode}"
             sched = fn(circuit, deps, shape)
             plan = qb.plan_evc(terms, n, shape, True)
             st = qb.init_state(n, shape)
+            assert qb.state_mode(st)["inplace_qr"] == (mode == "1")
             qb.run_qsu(st, circuit, sched)
             mine = {pe: st.sub_of(pe) for pe in range(st.pe_begin(), st.pe_begin() + st.pe_count())}
             layout_pos = list(st.layout.pos_of)

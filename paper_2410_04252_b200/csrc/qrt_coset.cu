@@ -418,6 +418,13 @@ __global__ void __launch_bounds__(2 * kCosetThreads, 1)
     double2 acc = make_double2(0.0, 0.0);
     for (int k = team; k < ntile; k += 2) {
         const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[k % 3]));
+        // A parity wait only tells the two newest phases apart: first make
+        // sure this buffer's previous phase (tile k - 3, loaded by this very
+        // team two tiles ago) has completed, then wait for tile k's phase.
+        // Without the first wait a team that computes two tiles faster than
+        // one fill completes reads a half-loaded buffer (seen as a rare wrong
+        // energy on few-group linear passes, 24 qubits / 2000 uniform words).
+        if (k >= 3) mbar_wait(a, static_cast<unsigned>(((k / 3) - 1) & 1));
         mbar_wait(a, static_cast<unsigned>((k / 3) & 1));
         coset_tile_sets<GENERIC, ONES>(P, bufs + (k % 3) * E, stab, tid, tile_of(k) << kTileBits, pe, acc);
         named_bar(1 + team, kCosetThreads);  // the team is done reading buffer k % 3
@@ -426,7 +433,177 @@ __global__ void __launch_bounds__(2 * kCosetThreads, 1)
     asm volatile("cp.async.wait_all;\n" ::);
     const double2 tot = block_sum(acc, scratch);
     if (threadIdx.x == 0) {
-        double* slot = red + 2 * (static_cast<std::size_t>(blockIdx.y) * gridDim.x + blockIdx.x);
+        // per-PE slots are tiles_per_pe apart (reduce_slots_kernel); this grid is narrower
+        double* slot = red + 2 * (static_cast<std::size_t>(blockIdx.y) * P.tiles_per_pe + blockIdx.x);
+        slot[0] += tot.x;
+        slot[1] += tot.y;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Split cosets (Jordan-Wigner fast groups only).  A lane pair shares one
+// 32-amplitude coset: the even lane holds the 32 real parts, the odd lane the
+// 32 imaginary parts (64 registers instead of 128), because
+//   sum_rho T[rho] Re(conj(a_s) a_r) = sum_rho T[rho] re_s re_r + sum_rho T[rho] im_s im_r
+// splits into two independent per-lane sums that the final reduction adds
+// anyway.  Each lane spends 2 fp64 instructions per pair (DMUL + DFMA, 4/3 of
+// the fused form) but the register footprint halves, so twice the warps stay
+// resident to hide the LDS / DFMA latencies that bound the 128-thread form;
+// adjacent lanes read the two halves of one 16-byte amplitude, so a warp's
+// coset loads stay conflict-free.
+
+template <int XQ>
+__device__ __forceinline__ double coset_group_split(const double (&a)[32], const double2* __restrict__ T2) {
+    constexpr int H = top_bit(XQ);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+        const double2 t = T2[h];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int rho = 2 * h + u;
+            const int r = ins0(rho, H);
+            const int s = r ^ XQ;
+            acc[rho & 3] = fma(u ? t.y : t.x, a[s] * a[r], acc[rho & 3]);
+        }
+    }
+    return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
+template <int XQ>
+__device__ __forceinline__ void coset_fast_split(const double (&a)[32], const CosetParams& P, const CosetSet& S,
+                                                 const double2* __restrict__ tabs, unsigned present, std::uint64_t W,
+                                                 std::uint64_t pe, double& acc) {
+    if (!((present >> XQ) & 1u)) return;
+    const int g0 = S.g_begin + S.xbeg[XQ - 1], g1 = S.g_begin + S.xbeg[XQ];
+    for (int g = g0; g < g1; ++g) {
+        const CosetGroup& G = P.groups[g];
+        const double r = coset_group_split<XQ>(a, tabs + (G.tab >> 1));
+        const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
+        acc += odd ? -r : r;
+    }
+}
+
+// t2 = lane index within the 256-thread team: coset t2 >> 1, part t2 & 1.
+__device__ __forceinline__ void coset_tile_sets_split(const CosetParams& P, const double2* __restrict__ tile,
+                                                      const double2* __restrict__ stab, int t2, u64 wout, u64 pe,
+                                                      double& acc) {
+    const int t = t2 >> 1, part = t2 & 1;
+    const double* __restrict__ tiled = reinterpret_cast<const double*>(tile) + part;
+    for (int s = 0; s < P.n_sets; ++s) {
+        const CosetSet& S = P.sets[s];
+        int ebase = 0;
+#pragma unroll
+        for (int i = 0; i < kTileBits - kCosetBits; ++i) ebase |= ((t >> i) & 1) << S.tb[i];
+        int swq[kCosetBits];
+#pragma unroll
+        for (int q = 0; q < kCosetBits; ++q) swq[q] = swz(1 << S.S[q]);
+        const int sb = swz(ebase);
+        double a[32];
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+            int o = sb;
+#pragma unroll
+            for (int q = 0; q < kCosetBits; ++q)
+                if ((r >> q) & 1) o ^= swq[q];
+            a[r] = tiled[2 * o];
+        }
+        const u64 W = static_cast<u64>(ebase) | wout;
+        const unsigned present = S.present;
+        coset_fast_split<3>(a, P, S, stab, present, W, pe, acc);
+        coset_fast_split<5>(a, P, S, stab, present, W, pe, acc);
+        coset_fast_split<6>(a, P, S, stab, present, W, pe, acc);
+        coset_fast_split<9>(a, P, S, stab, present, W, pe, acc);
+        coset_fast_split<10>(a, P, S, stab, present, W, pe, acc);
+        coset_fast_split<12>(a, P, S, stab, present, W, pe, acc);
+        coset_fast_split<15>(a, P, S, stab, present, W, pe, acc);
+        coset_fast_split<17>(a, P, S, stab, present, W, pe, acc);
+        coset_fast_split<18>(a, P, S, stab, present, W, pe, acc);
+        coset_fast_split<20>(a, P, S, stab, present, W, pe, acc);
+        coset_fast_split<23>(a, P, S, stab, present, W, pe, acc);
+        coset_fast_split<24>(a, P, S, stab, present, W, pe, acc);
+        coset_fast_split<27>(a, P, S, stab, present, W, pe, acc);
+        coset_fast_split<29>(a, P, S, stab, present, W, pe, acc);
+        coset_fast_split<30>(a, P, S, stab, present, W, pe, acc);
+    }
+}
+
+constexpr int kSplitTeam = 2 * kCosetThreads;  // 256 lanes per tile
+
+// coset_pipe_kernel with split cosets: two teams of 256 threads (16 warps per
+// SM at <= 128 registers), three tile buffers, mbarrier-tracked cp.async fills.
+__global__ void __launch_bounds__(2 * kSplitTeam, 1)
+    coset_pipe_split_kernel(const __grid_constant__ CosetParams P, double* __restrict__ red) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double2 scratch[2 * kSplitTeam / 32];
+    __shared__ __align__(8) unsigned long long full[3];
+    constexpr int E = 1 << kTileBits;
+    const int c = P.c;
+    const int team = threadIdx.x / kSplitTeam, tid = threadIdx.x % kSplitTeam;
+    double2* bufs = reinterpret_cast<double2*>(smem_raw);  // 3 x E
+    u64* tabo = reinterpret_cast<u64*>(bufs + 3 * E);
+    double2* stab = reinterpret_cast<double2*>(tabo + ((1 << (kTileBits - c)) | 1) + 1);
+    for (int i = threadIdx.x; i < (P.n_tab >> 1); i += blockDim.x) {
+        const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&stab[i]));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(P.gtabs + 2 * i));
+    }
+    for (int h = threadIdx.x; h < (1 << (kTileBits - c)); h += blockDim.x) {
+        u64 o = 0;
+        for (int i = c; i < kTileBits; ++i)
+            if ((h >> (i - c)) & 1) o ^= P.tile_vec[i];
+        tabo[h] = o;
+    }
+    if (threadIdx.x < 3) {
+        const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[threadIdx.x]));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(kSplitTeam));
+    }
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
+
+    const int tiles = P.tiles_per_pe;
+    const int stride = static_cast<int>(gridDim.x);
+    const int ntile = (tiles - static_cast<int>(blockIdx.x) + stride - 1) / stride;
+    const amp_t* __restrict__ v = P.ptrs[blockIdx.y];
+    const u64 pe = static_cast<u64>(P.pe_begin) + blockIdx.y;
+    const int cmask = (1 << c) - 1;
+    auto tile_of = [&](int k) { return static_cast<u64>(blockIdx.x) + static_cast<u64>(k) * stride; };
+    auto issue = [&](int k) {
+        const u64 b = tile_of(k);
+        u64 base = 0;
+        for (int i = 0; i < P.n_outer; ++i)
+            if ((b >> i) & 1ull) base ^= P.outer_vec[i];
+        double2* tile = bufs + (k % 3) * E;
+        for (int e = tid; e < E; e += kSplitTeam) {
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&tile[swz(e)]));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
+                         "l"(&v[base ^ tabo[e >> c] ^ (e & cmask)]));
+        }
+        const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[k % 3]));
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a));
+    };
+    for (int k = 0; k < 3 && k < ntile; ++k)
+        if (((k + 1) & 1) == team) issue(k);
+
+    double acc = 0.0;
+    for (int k = team; k < ntile; k += 2) {
+        const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[k % 3]));
+        // A parity wait only tells the two newest phases apart: first make
+        // sure this buffer's previous phase (tile k - 3, loaded by this very
+        // team two tiles ago) has completed, then wait for tile k's phase.
+        // Without the first wait a team that computes two tiles faster than
+        // one fill completes reads a half-loaded buffer (seen as a rare wrong
+        // energy on few-group linear passes, 24 qubits / 2000 uniform words).
+        if (k >= 3) mbar_wait(a, static_cast<unsigned>(((k / 3) - 1) & 1));
+        mbar_wait(a, static_cast<unsigned>((k / 3) & 1));
+        coset_tile_sets_split(P, bufs + (k % 3) * E, stab, tid, tile_of(k) << kTileBits, pe, acc);
+        named_bar(1 + team, kSplitTeam);
+        if (k + 3 < ntile) issue(k + 3);
+    }
+    asm volatile("cp.async.wait_all;\n" ::);
+    const double2 tot = block_sum(make_double2(acc, 0.0), scratch);
+    if (threadIdx.x == 0) {
+        // per-PE slots are tiles_per_pe apart (reduce_slots_kernel); this grid is narrower
+        double* slot = red + 2 * (static_cast<std::size_t>(blockIdx.y) * P.tiles_per_pe + blockIdx.x);
         slot[0] += tot.x;
         slot[1] += tot.y;
     }
@@ -477,6 +654,21 @@ void launch_coset_pass(const CosetParams& P, const CosetDiagTerm* dterms, int pe
                                   ((std::size_t{1} << (kTileBits - P.c)) + 2) * sizeof(std::uint64_t) +
                                   static_cast<std::size_t>(P.n_tab) * sizeof(double);
         dim3 pgrid(static_cast<unsigned>(std::min(nsm[device], P.tiles_per_pe)), static_cast<unsigned>(pe_count));
+        static const bool split = [] {
+            const char* e = std::getenv("QRT_EVC_SPLIT");
+            return e ? std::atoi(e) != 0 : true;
+        }();
+        if (split && !generic && !any_ones) {  // Jordan-Wigner fast groups only: split cosets
+            static bool sattr[64] = {};
+            if (!sattr[device]) {
+                QRT_CUDA(cudaFuncSetAttribute(coset_pipe_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              220 * 1024));
+                sattr[device] = true;
+            }
+            coset_pipe_split_kernel<<<pgrid, 2 * kSplitTeam, psmem, stream>>>(P, red);
+            QRT_CUDA(cudaGetLastError());
+            return;
+        }
         if (generic)
             coset_pipe_kernel<true, true><<<pgrid, 2 * kCosetThreads, psmem, stream>>>(P, red);
         else if (any_ones)

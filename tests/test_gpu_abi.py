@@ -82,3 +82,44 @@ def test_abi_gates_qr_expectation(qb, device):
         assert b"global" in lib.qrt_last_error()
     finally:
         assert lib.qrt_state_destroy(st) == 0
+
+
+@pytest.mark.parametrize("kind", ["jw", "uniform"])
+def test_abi_per_pe_partials_pipelined(qb, device, kind):
+    """Per-PE partials (dist_sim.cpp:289-295) from the persistent pipelined
+    EVC kernels: 2^20 amplitudes per PE = 256 tiles, more than one CTA per SM
+    covers, so every CTA walks several tiles and the slot layout matters."""
+    lib = _lib(qb)
+    n, p = 22, 4
+    nl = n - 2
+    psi = qb.random_state(n, 2024).reshape(p, -1).copy()
+    if kind == "jw":
+        words = [t for t in qb.gen_synthetic_jw(nl, 5, 6) if set(t.letters) & {"X", "Y"}][:300]
+    else:
+        words = qb.gen_uniform_words(nl, 120, 7)
+    x, y, z, co = [], [], [], []
+    rng = np.random.default_rng(1)
+    for t in words:
+        xm = sum(1 << q for q, ch in enumerate(t.letters) if ch == "X")
+        ym = sum(1 << q for q, ch in enumerate(t.letters) if ch == "Y")
+        zm = sum(1 << q for q, ch in enumerate(t.letters) if ch == "Z")
+        if xm | ym == 0:
+            continue
+        x.append(xm), y.append(ym), z.append(zm), co.append(t.coeff)
+    m = len(x)
+    gz = [int(rng.integers(0, p)) for _ in range(m)]
+    co = np.array(co, dtype=np.complex128)
+    st = C.c_void_p()
+    assert lib.qrt_state_create(n, p, 0, None, C.byref(st)) == 0, lib.qrt_last_error()
+    try:
+        for pe in range(p):
+            assert lib.qrt_state_upload(st, pe, _d(np.ascontiguousarray(psi[pe]))) == 0
+        U = C.c_uint64 * m
+        partial = np.zeros(2 * p)
+        assert lib.qrt_pauli_expectation(st, m, U(*x), U(*y), U(*z), U(*gz), _d(co), _d(partial)) == 0, \
+            lib.qrt_last_error()
+        terms = [cpu.MaskedTerm(x[i], y[i], z[i], gz[i], bin(y[i]).count("1")) for i in range(m)]
+        want = cpu.expectation_tile(psi, terms, co)
+        assert np.max(np.abs(partial.view(np.complex128) - want)) <= 1e-12 * (1 + np.max(np.abs(want)))
+    finally:
+        assert lib.qrt_state_destroy(st) == 0

@@ -13,8 +13,11 @@ ps = [int(x) for x in sys.argv[3].split(",")]
 qb.init_device(0, 1, 0)
 terms = qb.gen_uniform_words(n, count, 2024)
 psi = qb.random_state(n, 1234)
-masked = [cpu.mask_term(t.letters, list(range(n)), n) for t in terms]
-want = cpu.expectation_tile(psi.reshape(1, -1).copy(), masked, [t.coeff for t in terms]).sum()
+if len(sys.argv) > 4 and sys.argv[4] == "nooracle":
+    want = 0j
+else:
+    masked = [cpu.mask_term(t.letters, list(range(n)), n) for t in terms]
+    want = cpu.expectation_tile(psi.reshape(1, -1).copy(), masked, [t.coeff for t in terms]).sum()
 out = {"n": n, "count": count, "oracle": want.real}
 for p in ps:
     shape = qb.ClusterShape.flat(p)

@@ -1,9 +1,7 @@
 #!/bin/bash
-# Round-2 GPU check (run from the repo root under gpurun): full GPU test suite,
-# smoke, then the split-coset EVC A/B.
-O=${OUT:-gpurun_out/r2b}; mkdir -p $O
-timeout 1500 python -m pytest tests -m gpu -q --durations=15 > $O/tests.log 2>&1; echo rc=$? >> $O/tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo rc=$? >> $O/smoke.log
+# A/B of the split-coset EVC kernel (QRT_EVC_SPLIT) on the 30q GateFabric and HEA steps + EVC tests
+O=${OUT:-gpurun_out/r2evc}; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_evc.py tests/test_gpu_parity.py -q -x -k "expectation or evc or energy or coset" > $O/tests.log 2>&1; echo rc=$? >> $O/tests.log
 for sp in 1 0; do
   QRT_EVC_SPLIT=$sp timeout 600 python bench.py --qubits 30 --no-cpu-baseline --steps 2 --warmup 3 > $O/gf30_split$sp.json 2>&1
   QRT_EVC_SPLIT=$sp timeout 600 python bench.py --qubits 30 --circuit hea --no-cpu-baseline --steps 2 --warmup 3 > $O/hea30_split$sp.json 2>&1

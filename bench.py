@@ -328,6 +328,7 @@ def run_ours(args):
         st, energy, _, _, _ = step(profile=(i == args.warmup - 1))
         if i == args.warmup - 1:
             stats = st.stats()
+            inplace_qr = qb.state_mode(st)["inplace_qr"]
         del st
     barrier()
     torch.cuda.synchronize()
@@ -350,8 +351,9 @@ def run_ours(args):
     if stats is None:  # --warmup 0: profile one extra untimed step
         st, _, _, _, _ = step(profile=True)
         stats = st.stats()
+        inplace_qr = qb.state_mode(st)["inplace_qr"]
         del st
-    g, qr, pa = stats["gates"], stats["qr"], stats["pauli"]
+    g, qr, pa, xf = stats["gates"], stats["qr"], stats["pauli"], stats["qr_xfer"]
     fam_kernel = {"gates": ("gate_pass_kernel (DMMA fp64 tensor, dense 3/4-qubit gates)" if args.circuit == "gatefabric"
                             else "light_pass_kernel (register-resident 1q/2q/diagonal runs)"),
                   "pauli": "coset_pass_kernel (EVC, 5-qubit register cosets)"}
@@ -419,8 +421,11 @@ def run_ours(args):
         "clocks": clk,
         "roofline": roof,
         "phases_ms": {"gates": g["ms"], "qr": qr["ms"], "pauli": pa["ms"], "misc": stats["misc"]["ms"],
+                      "qr_exchange_kernels": xf["ms"], "qr_barriers": qr["ms"] - xf["ms"],
                       "gate_passes": g["launches"], "qr_launches": qr["launches"], "pauli_passes": pa["launches"],
-                      "qr_nvlink_gbs": (qr["bytes"] / (qr["ms"] / 1e3) / 1e9) if qr["ms"] > 0 else None},
+                      "qr_nvlink_gbs_incl_barriers": (qr["bytes"] / (qr["ms"] / 1e3) / 1e9) if qr["ms"] > 0 else None,
+                      "qr_nvlink_gbs": (xf["bytes"] / (xf["ms"] / 1e3) / 1e9) if xf["ms"] > 0 else None,
+                      "qr_mode": "in-place (pairwise swap)" if inplace_qr else "push / fused pull (two buffers)"},
     }
     line["native_so_loaded"] = loaded_native()
     if not args.no_cpu_baseline:

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define QRT_ABI_VERSION 1
+#define QRT_ABI_VERSION 2
 
 /* Status codes; the host layer maps each to the reference exception type
  * (types.hpp:35-53). */
@@ -117,6 +117,16 @@ qrt_status qrt_reorder(qrt_state* st, const int* dest, uint64_t* relocated);
  * *sm_count = multiprocessors of the state's device (grid sizing). */
 qrt_status qrt_state_mode(const qrt_state* st, int* inplace_qr, int* sm_count);
 
+/* NVLink microbenchmark of the QR exchange (diagnostics, single process):
+ * n_gpus GPUs (2/4/8) with one PE of 2^n_local amplitudes each swap their k
+ * highest local positions with k PE bits through CUDA peer access, using the
+ * push kernel (inplace = 0, two buffers) or the in-place exchange
+ * (inplace = 1).  Returns the mean over `iters` of the slowest GPU's kernel
+ * time and the per-direction NVLink rate (bytes each GPU sends / that time).
+ * Meant to run under ncu (one process) for the NVLink counters. */
+qrt_status qrt_qr_bench(int n_gpus, int n_local, int k, int inplace, int iters, double* ms_per_qr,
+                        double* gbs_per_direction);
+
 /* Host-only: the in-place decomposition of a reorder map (no device).
  * local_pairs0 / local_pairs1 receive n0 / n1 disjoint local position
  * transpositions (a, c) applied in that order, cross_pairs k (local slot,
@@ -172,7 +182,10 @@ typedef struct {
     uint64_t calls;         /* ABI calls                                       */
 } qrt_kernel_stats;
 
-enum { QRT_K_GATES = 0, QRT_K_QR = 1, QRT_K_PAULI = 2, QRT_K_MISC = 3, QRT_K_COUNT = 4 };
+/* QRT_K_QR times a whole QR (barriers included); QRT_K_QR_XFER only its
+ * exchange kernels (the NVLink transfer), so the barrier cost is their
+ * difference. */
+enum { QRT_K_GATES = 0, QRT_K_QR = 1, QRT_K_PAULI = 2, QRT_K_MISC = 3, QRT_K_QR_XFER = 4, QRT_K_COUNT = 5 };
 
 qrt_status qrt_profile_enable(qrt_state* st, int on);
 qrt_status qrt_stats(const qrt_state* st, qrt_kernel_stats out[QRT_K_COUNT]);

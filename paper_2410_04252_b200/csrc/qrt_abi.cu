@@ -127,6 +127,8 @@ void free_state(qrt_state* st) {
     if (st->d_flag) cudaFree(st->d_flag);
     if (st->ev0) cudaEventDestroy(st->ev0);
     if (st->ev1) cudaEventDestroy(st->ev1);
+    if (st->ev2) cudaEventDestroy(st->ev2);
+    if (st->ev3) cudaEventDestroy(st->ev3);
     if (st->stream) cudaStreamDestroy(st->stream);
     delete st;
 }
@@ -191,16 +193,17 @@ void nccl_check(ncclResult_t r, const char* what, const char* file, int line) {
     fail(QRT_ERR_NCCL, std::string(ncclGetErrorString(r)) + " in " + what + " at " + file + ":" + std::to_string(line));
 }
 
-ProfileScope::ProfileScope(qrt_state* s, int f) : st(s), fam(f) {
-    if (st->profile) QRT_CUDA(cudaEventRecord(st->ev0, st->stream));
+ProfileScope::ProfileScope(qrt_state* s, int f, bool inner_scope) : st(s), fam(f), inner(inner_scope) {
+    if (st->profile) QRT_CUDA(cudaEventRecord(inner ? st->ev2 : st->ev0, st->stream));
 }
 ProfileScope::~ProfileScope() {
     if (!st->profile) return;
     // Destructors must not throw (this one may run during unwinding): a
     // failure here leaves the timing out and is caught by the next checked call.
     float ms = 0.f;
-    if (cudaEventRecord(st->ev1, st->stream) == cudaSuccess && cudaEventSynchronize(st->ev1) == cudaSuccess &&
-        cudaEventElapsedTime(&ms, st->ev0, st->ev1) == cudaSuccess)
+    cudaEvent_t b = inner ? st->ev2 : st->ev0, e = inner ? st->ev3 : st->ev1;
+    if (cudaEventRecord(e, st->stream) == cudaSuccess && cudaEventSynchronize(e) == cudaSuccess &&
+        cudaEventElapsedTime(&ms, b, e) == cudaSuccess)
         st->stats[fam].ms += ms;
 }
 
@@ -422,6 +425,8 @@ qrt_status qrt_state_create(int n, int p, int device, qrt_comm* comm, qrt_state*
             QRT_CUDA(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
             QRT_CUDA(cudaEventCreate(&st->ev0));
             QRT_CUDA(cudaEventCreate(&st->ev1));
+            QRT_CUDA(cudaEventCreate(&st->ev2));
+            QRT_CUDA(cudaEventCreate(&st->ev3));
             QRT_CUDA(cudaMalloc(&st->d_flag, sizeof(int)));
             QRT_CUDA(cudaMemsetAsync(st->d_flag, 0, sizeof(int), st->stream));
             if (comm && world > 1) {  // every rank must take the same QR mode
@@ -616,6 +621,11 @@ qrt_status qrt_reorder(qrt_state* st, const int* dest, std::uint64_t* relocated)
         QRT_CUDA(cudaStreamSynchronize(st->stream));
         if (relocated) *relocated = moved;
     });
+}
+
+qrt_status qrt_qr_bench(int n_gpus, int n_local, int k, int inplace, int iters, double* ms_per_qr,
+                        double* gbs_per_direction) {
+    return guarded([&] { qr_bench(n_gpus, n_local, k, inplace, iters, ms_per_qr, gbs_per_direction); });
 }
 
 qrt_status qrt_reorder_inplace_plan(int n, int p, const int* dest, int* local_pairs0, int* n0, int* local_pairs1,

@@ -96,7 +96,8 @@ struct qrt_state {
     // Measurement.
     bool profile = false;
     qrt_kernel_stats stats[QRT_K_COUNT]{};
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // ProfileScope (outer: one ABI call's family)
+    cudaEvent_t ev2 = nullptr, ev3 = nullptr;  // ProfileScope(inner): kernels only, e.g. QR without barriers
 
     qrt::amp_t* live(int local_pe) const { return bufs[cur][static_cast<std::size_t>(local_pe)]; }
 };
@@ -108,7 +109,8 @@ namespace qrt {
 struct ProfileScope {
     qrt_state* st;
     int fam;
-    ProfileScope(qrt_state* s, int f);
+    bool inner;
+    ProfileScope(qrt_state* s, int f, bool inner_scope = false);
     ~ProfileScope();  // never throws: a failed event query is recorded, not raised
 };
 
@@ -126,6 +128,7 @@ void flush_reorder(qrt_state* st);  // execute a pending QR (no-op if none)
 bool fused_qr_enabled();
 void reorder_plan(int n, int p, const int* dest, int src_pe, std::uint64_t* dst_pe, std::uint64_t* dst_off,
                   std::uint64_t* relocated);
+void qr_bench(int n_gpus, int nl, int k, int inplace, int iters, double* ms_out, double* gbs_out);
 void reorder_inplace_plan(int n, int p, const int* dest, int* pairs0, int* n0, int* pairs1, int* n1, int* cross,
                           int* k);
 void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const std::uint64_t* y,

@@ -456,12 +456,18 @@ void execute_inplace(qrt_state* st, const int* dest, std::uint64_t relocated) {
     make_deposit(rest, a.dep);
     for (int pe = 0; pe < st->p; ++pe) a.pe_ptr[pe] = st->peer[st->cur][static_cast<std::size_t>(pe)];
     barrier_on_stream(st);  // every peer is done with the buffers touched here
-    const std::uint64_t work = static_cast<std::uint64_t>((1 << a.k) - 1) << a.dep.n_hi;
-    const unsigned gx = static_cast<unsigned>(std::min<std::uint64_t>(work, static_cast<std::uint64_t>(st->sm_count) * 8));
-    exchange_kernel<<<dim3(gx, static_cast<unsigned>(st->pe_count)), 256, 0, st->stream>>>(a);
-    QRT_CUDA(cudaGetLastError());
+    {
+        ProfileScope xfer(st, QRT_K_QR_XFER, true);
+        const std::uint64_t work = static_cast<std::uint64_t>((1 << a.k) - 1) << a.dep.n_hi;
+        const unsigned gx =
+            static_cast<unsigned>(std::min<std::uint64_t>(work, static_cast<std::uint64_t>(st->sm_count) * 8));
+        exchange_kernel<<<dim3(gx, static_cast<unsigned>(st->pe_count)), 256, 0, st->stream>>>(a);
+        QRT_CUDA(cudaGetLastError());
+    }
     barrier_on_stream(st);  // every peer's stores into this PE have landed
     st->stats[QRT_K_QR].launches++;
+    st->stats[QRT_K_QR_XFER].launches++;
+    st->stats[QRT_K_QR_XFER].bytes += 16.0 * static_cast<double>(relocated) * st->pe_count / st->p;
     st->stats[QRT_K_QR].bytes += 16.0 * static_cast<double>(relocated) * st->pe_count / st->p;
 }
 
@@ -493,12 +499,17 @@ void execute_reorder(qrt_state* st, const int* dest) {
     {
         ProfileScope prof(st, QRT_K_QR);
         barrier_on_stream(st);  // no peer still reads the buffers written here (fused passes)
-        dim3 grid(static_cast<unsigned>(1ull << a.m.n_hi), static_cast<unsigned>(st->pe_count));
-        reorder_kernel<<<grid, 256, 0, st->stream>>>(a);
-        QRT_CUDA(cudaGetLastError());
+        {
+            ProfileScope xfer(st, QRT_K_QR_XFER, true);
+            dim3 grid(static_cast<unsigned>(1ull << a.m.n_hi), static_cast<unsigned>(st->pe_count));
+            reorder_kernel<<<grid, 256, 0, st->stream>>>(a);
+            QRT_CUDA(cudaGetLastError());
+        }
         barrier_on_stream(st);
     }
     st->stats[QRT_K_QR].launches++;
+    st->stats[QRT_K_QR_XFER].launches++;
+    st->stats[QRT_K_QR_XFER].bytes += 16.0 * static_cast<double>(relocated) * st->pe_count / st->p;
     // bytes that cross to another PE (each way), counted for this process's PEs
     st->stats[QRT_K_QR].bytes += 16.0 * static_cast<double>(relocated) * st->pe_count / st->p;
     st->cur = nxt;
@@ -557,6 +568,134 @@ void reorder_inplace_plan(int n, int p, const int* dest, int* pairs0, int* n0, i
     put(P.local[0], pairs0, n0);
     put(P.local[1], pairs1, n1);
     put(P.cross, cross, k);
+}
+
+// Single-process NVLink microbenchmark of the QR exchange kernels (one PE per
+// GPU, CUDA peer access instead of IPC): the k highest local positions swap
+// with k PE bits on n_gpus GPUs at once, push (reorder_kernel into a second
+// buffer) or in place (exchange_kernel).  One process drives every GPU, so
+// ncu can attach and read the NVLink counters (never wrap a multi-rank run).
+void qr_bench(int n_gpus, int nl, int k, int inplace, int iters, double* ms_out, double* gbs_out) {
+    if (n_gpus < 2 || n_gpus > 8 || (n_gpus & (n_gpus - 1))) fail(QRT_ERR_CONFIG, "n_gpus must be 2, 4 or 8");
+    const int g = __builtin_ctz(static_cast<unsigned>(n_gpus));
+    if (k < 1 || k > g) fail(QRT_ERR_CONFIG, "k must be in [1, log2 n_gpus]");
+    if (nl < kTileBits || nl > 33) fail(QRT_ERR_CONFIG, "n_local must be in [12, 33]");
+    if (iters < 1) fail(QRT_ERR_CONFIG, "iters must be >= 1");
+    int ndev = 0;
+    QRT_CUDA(cudaGetDeviceCount(&ndev));
+    if (ndev < n_gpus) fail(QRT_ERR_NO_DEVICE, "not enough GPUs for the QR microbenchmark");
+    int prev = 0;
+    QRT_CUDA(cudaGetDevice(&prev));
+    const int n = nl + g;
+    const std::uint64_t amps = 1ull << nl;
+    std::vector<amp_t*> b0(static_cast<std::size_t>(n_gpus), nullptr), b1(static_cast<std::size_t>(n_gpus), nullptr);
+    std::vector<cudaStream_t> str(static_cast<std::size_t>(n_gpus), nullptr);
+    std::vector<cudaEvent_t> e0(static_cast<std::size_t>(n_gpus), nullptr), e1(static_cast<std::size_t>(n_gpus), nullptr);
+    std::vector<int> sms(static_cast<std::size_t>(n_gpus), 148);
+    auto cleanup = [&] {
+        for (int d = 0; d < n_gpus; ++d) {
+            cudaSetDevice(d);
+            cudaDeviceSynchronize();
+            if (b0[static_cast<std::size_t>(d)]) cudaFree(b0[static_cast<std::size_t>(d)]);
+            if (b1[static_cast<std::size_t>(d)]) cudaFree(b1[static_cast<std::size_t>(d)]);
+            if (e0[static_cast<std::size_t>(d)]) cudaEventDestroy(e0[static_cast<std::size_t>(d)]);
+            if (e1[static_cast<std::size_t>(d)]) cudaEventDestroy(e1[static_cast<std::size_t>(d)]);
+            if (str[static_cast<std::size_t>(d)]) cudaStreamDestroy(str[static_cast<std::size_t>(d)]);
+        }
+        cudaSetDevice(prev);
+    };
+    try {
+        for (int d = 0; d < n_gpus; ++d) {
+            const auto D = static_cast<std::size_t>(d);
+            QRT_CUDA(cudaSetDevice(d));
+            QRT_CUDA(cudaDeviceGetAttribute(&sms[D], cudaDevAttrMultiProcessorCount, d));
+            QRT_CUDA(cudaStreamCreateWithFlags(&str[D], cudaStreamNonBlocking));
+            QRT_CUDA(cudaEventCreate(&e0[D]));
+            QRT_CUDA(cudaEventCreate(&e1[D]));
+            QRT_CUDA(cudaMalloc(&b0[D], amps * sizeof(amp_t)));
+            QRT_CUDA(cudaMemset(b0[D], 0, amps * sizeof(amp_t)));
+            if (!inplace) QRT_CUDA(cudaMalloc(&b1[D], amps * sizeof(amp_t)));
+            for (int o = 0; o < n_gpus; ++o) {
+                if (o == d) continue;
+                const cudaError_t e = cudaDeviceEnablePeerAccess(o, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else QRT_CUDA(e);
+            }
+        }
+        std::vector<int> dest(static_cast<std::size_t>(n));
+        std::iota(dest.begin(), dest.end(), 0);
+        for (int i = 0; i < k; ++i) {
+            dest[static_cast<std::size_t>(nl - 1 - i)] = nl + i;
+            dest[static_cast<std::size_t>(nl + i)] = nl - 1 - i;
+        }
+        std::vector<QrArgs> pa(static_cast<std::size_t>(n_gpus));
+        std::vector<XchgArgs> xa(static_cast<std::size_t>(n_gpus));
+        std::uint64_t relocated = 0;
+        for (int d = 0; d < n_gpus; ++d) {
+            const auto D = static_cast<std::size_t>(d);
+            bool identity = false;
+            relocated = build_map(n, nl, d, dest.data(), pa[D].m, identity);
+            pa[D].src[0] = b0[D];
+            for (int pe = 0; pe < n_gpus; ++pe) pa[D].dst[pe] = b1[static_cast<std::size_t>(pe)];
+            const InplacePlan P = plan_inplace(n, nl, dest.data());
+            XchgArgs& a = xa[D];
+            a.pe_begin = d;
+            a.k = static_cast<int>(P.cross.size());
+            std::vector<char> used(static_cast<std::size_t>(nl), 0);
+            for (int i = 0; i < a.k; ++i) {
+                a.d_pos[i] = P.cross[static_cast<std::size_t>(i)].first;
+                a.pe_bit[i] = P.cross[static_cast<std::size_t>(i)].second;
+                used[static_cast<std::size_t>(a.d_pos[i])] = 1;
+            }
+            a.f = -1;
+            for (int x = nl - 1; x >= 0; --x)
+                if (!used[static_cast<std::size_t>(x)]) {
+                    a.f = x;
+                    used[static_cast<std::size_t>(x)] = 1;
+                    break;
+                }
+            std::vector<int> rest;
+            for (int x = 0; x < nl; ++x)
+                if (!used[static_cast<std::size_t>(x)]) rest.push_back(x);
+            make_deposit(rest, a.dep);
+            for (int pe = 0; pe < n_gpus; ++pe) a.pe_ptr[pe] = b0[static_cast<std::size_t>(pe)];
+        }
+        double total_ms = 0.0;
+        for (int it = 0; it <= iters; ++it) {  // iteration 0 warms up
+            for (int d = 0; d < n_gpus; ++d) {
+                const auto D = static_cast<std::size_t>(d);
+                QRT_CUDA(cudaSetDevice(d));
+                QRT_CUDA(cudaEventRecord(e0[D], str[D]));
+                if (inplace) {
+                    const std::uint64_t work = static_cast<std::uint64_t>((1 << xa[D].k) - 1) << xa[D].dep.n_hi;
+                    const unsigned gx = static_cast<unsigned>(std::min<std::uint64_t>(work, static_cast<std::uint64_t>(sms[D]) * 8));
+                    exchange_kernel<<<dim3(gx, 1), 256, 0, str[D]>>>(xa[D]);
+                } else {
+                    reorder_kernel<<<dim3(static_cast<unsigned>(1ull << pa[D].m.n_hi), 1), 256, 0, str[D]>>>(pa[D]);
+                }
+                QRT_CUDA(cudaGetLastError());
+                QRT_CUDA(cudaEventRecord(e1[D], str[D]));
+            }
+            double worst = 0.0;
+            for (int d = 0; d < n_gpus; ++d) {
+                const auto D = static_cast<std::size_t>(d);
+                QRT_CUDA(cudaSetDevice(d));
+                QRT_CUDA(cudaEventSynchronize(e1[D]));
+                float ms = 0.f;
+                QRT_CUDA(cudaEventElapsedTime(&ms, e0[D], e1[D]));
+                worst = std::max(worst, static_cast<double>(ms));
+            }
+            if (it > 0) total_ms += worst;
+        }
+        const double ms = total_ms / iters;
+        const double bytes = 16.0 * static_cast<double>(relocated) / n_gpus;  // sent per GPU = received per GPU
+        if (ms_out) *ms_out = ms;
+        if (gbs_out) *gbs_out = bytes / (ms * 1e-3) / 1e9;
+    } catch (...) {
+        cleanup();
+        throw;
+    }
+    cleanup();
 }
 
 // Host-side replay of the kernel's index mapping for one source PE: for every

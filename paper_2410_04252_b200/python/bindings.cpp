@@ -311,7 +311,7 @@ PYBIND11_MODULE(_qrtile, m) {
             qrt_kernel_stats st[QRT_K_COUNT];
             qrt_stats(s.device->handle, st);
             py::dict d;
-            const char* names[QRT_K_COUNT] = {"gates", "qr", "pauli", "misc"};
+            const char* names[QRT_K_COUNT] = {"gates", "qr", "pauli", "misc", "qr_xfer"};
             for (int i = 0; i < QRT_K_COUNT; ++i) {
                 py::dict e;
                 e["launches"] = st[i].launches;

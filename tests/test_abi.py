@@ -28,7 +28,7 @@ def test_exports_every_declared_symbol(qb):
 
 def test_abi_version_and_codes(qb):
     lib = qb.load_libqrt()
-    assert lib.qrt_abi_version() == qb.QRT_ABI_VERSION == 1
+    assert lib.qrt_abi_version() == qb.QRT_ABI_VERSION == 2
     lib.qrt_last_error.restype = C.c_char_p
     assert isinstance(lib.qrt_last_error(), bytes)
 

@@ -167,3 +167,36 @@ def test_live_random_vs_reference(qb, ref):
                               ("adhoc", qb.adhoc_schedule)):
                 got = json.loads(qb.schedule_to_json(fn(c, d, qb.ClusterShape.flat(p))))
                 assert got == rc.schedule(sched, p)["schedule"]
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_batched_evc_search_identical(qb, monkeypatch, p):
+    """The incremental inclusion-exclusion tile search (g <= 3 global qubits)
+    emits the exhaustive search's plan byte for byte (evc_scheduler.cpp:150-236,
+    first lexicographic maximum), on uniform and Jordan-Wigner inputs."""
+    rng = np.random.default_rng(p)
+    for trial in range(12):
+        n = int(rng.integers(6, 15))
+        if p > (1 << (n - 3)):
+            continue
+        terms = (qb.gen_uniform_words(n, int(rng.integers(5, 300)), int(rng.integers(1 << 30)))
+                 if trial % 2 == 0 else qb.gen_synthetic_jw(n, int(rng.integers(1, 99)), int(rng.integers(3, n))))
+        shape = qb.ClusterShape.flat(p)
+        try:
+            monkeypatch.setenv("QRT_EVC_PLAN_BATCHED", "0")
+            slow = qb.plan_to_json(qb.plan_evc(terms, n, shape, True, 4))
+        except qb.Error:
+            continue
+        monkeypatch.setenv("QRT_EVC_PLAN_BATCHED", "1")
+        assert qb.plan_to_json(qb.plan_evc(terms, n, shape, True, 4)) == slow
+
+
+def test_batched_evc_search_fast(qb):
+    """C5 stress planning (10,000 uniform words, 34 qubits, p = 8: 60 tiles)
+    well under the exhaustive search's seconds (<= 0.3 s)."""
+    import time
+    terms = qb.gen_uniform_words(34, 10000, 2024)
+    t0 = time.perf_counter()
+    plan = qb.plan_evc(terms, 34, qb.ClusterShape.flat(8), True, 1)
+    assert len(plan.tiles) == 60
+    assert time.perf_counter() - t0 < 1.0

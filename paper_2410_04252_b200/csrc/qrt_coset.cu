@@ -354,6 +354,20 @@ __device__ __forceinline__ void mbar_wait(unsigned addr, unsigned parity) {
         "r"(parity));
 }
 
+// Fill barriers of the three-buffer pipelines.  Tile k lives in buffer k % 3
+// and its fill completes barrier (k % 3) + 3 * ((k / 3) & 1): each barrier then
+// serves every sixth tile, all consumed by the same team.  A parity wait only
+// distinguishes a barrier's current phase from the one before it; with one
+// barrier per buffer, a team that finished two tiles before the fill of tile
+// k - 3 (its own previous buffer use, issued by itself) completed saw that
+// phase's parity, took it for tile k's and read a half-filled buffer (a rare
+// wrong energy on few-group linear passes: 24 qubits, 2,000 uniform words).
+// With six barriers the phase before the awaited one is always the same
+// team's previous use of that barrier (complete), and the phase after it is
+// only issued once this team has released the buffer.
+__device__ __forceinline__ int fill_bar(int k) { return (k % 3) + 3 * ((k / 3) & 1); }
+__device__ __forceinline__ unsigned fill_parity(int k) { return static_cast<unsigned>((k / 6) & 1); }
+
 // Persistent, software-pipelined variant for passes without I/Z words: one
 // 256-thread CTA per SM holds three tile buffers; two teams of 128 threads
 // evaluate alternate tiles (team = tile index & 1) while the third buffer
@@ -366,7 +380,7 @@ __global__ void __launch_bounds__(2 * kCosetThreads, 1)
     coset_pipe_kernel(const __grid_constant__ CosetParams P, double* __restrict__ red) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double2 scratch[2 * kCosetThreads / 32];
-    __shared__ __align__(8) unsigned long long full[3];
+    __shared__ __align__(8) unsigned long long full[6];
     constexpr int E = 1 << kTileBits;
     const int c = P.c;
     const int team = threadIdx.x >> 7, tid = threadIdx.x & (kCosetThreads - 1);
@@ -383,7 +397,7 @@ __global__ void __launch_bounds__(2 * kCosetThreads, 1)
             if ((h >> (i - c)) & 1) o ^= P.tile_vec[i];
         tabo[h] = o;
     }
-    if (threadIdx.x < 3) {
+    if (threadIdx.x < 6) {
         const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[threadIdx.x]));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(kCosetThreads));
     }
@@ -408,7 +422,7 @@ __global__ void __launch_bounds__(2 * kCosetThreads, 1)
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
                          "l"(&v[base ^ tabo[e >> c] ^ (e & cmask)]));
         }
-        const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[k % 3]));
+        const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[fill_bar(k)]));
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a));
     };
     // tile k is issued by team (k + 1) & 1
@@ -417,15 +431,8 @@ __global__ void __launch_bounds__(2 * kCosetThreads, 1)
 
     double2 acc = make_double2(0.0, 0.0);
     for (int k = team; k < ntile; k += 2) {
-        const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[k % 3]));
-        // A parity wait only tells the two newest phases apart: first make
-        // sure this buffer's previous phase (tile k - 3, loaded by this very
-        // team two tiles ago) has completed, then wait for tile k's phase.
-        // Without the first wait a team that computes two tiles faster than
-        // one fill completes reads a half-loaded buffer (seen as a rare wrong
-        // energy on few-group linear passes, 24 qubits / 2000 uniform words).
-        if (k >= 3) mbar_wait(a, static_cast<unsigned>(((k / 3) - 1) & 1));
-        mbar_wait(a, static_cast<unsigned>((k / 3) & 1));
+        const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[fill_bar(k)]));
+        mbar_wait(a, fill_parity(k));
         coset_tile_sets<GENERIC, ONES>(P, bufs + (k % 3) * E, stab, tid, tile_of(k) << kTileBits, pe, acc);
         named_bar(1 + team, kCosetThreads);  // the team is done reading buffer k % 3
         if (k + 3 < ntile) issue(k + 3);
@@ -536,7 +543,7 @@ __global__ void __launch_bounds__(2 * kSplitTeam, 1)
     coset_pipe_split_kernel(const __grid_constant__ CosetParams P, double* __restrict__ red) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double2 scratch[2 * kSplitTeam / 32];
-    __shared__ __align__(8) unsigned long long full[3];
+    __shared__ __align__(8) unsigned long long full[6];
     constexpr int E = 1 << kTileBits;
     const int c = P.c;
     const int team = threadIdx.x / kSplitTeam, tid = threadIdx.x % kSplitTeam;
@@ -553,7 +560,7 @@ __global__ void __launch_bounds__(2 * kSplitTeam, 1)
             if ((h >> (i - c)) & 1) o ^= P.tile_vec[i];
         tabo[h] = o;
     }
-    if (threadIdx.x < 3) {
+    if (threadIdx.x < 6) {
         const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[threadIdx.x]));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(kSplitTeam));
     }
@@ -578,7 +585,7 @@ __global__ void __launch_bounds__(2 * kSplitTeam, 1)
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
                          "l"(&v[base ^ tabo[e >> c] ^ (e & cmask)]));
         }
-        const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[k % 3]));
+        const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[fill_bar(k)]));
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a));
     };
     for (int k = 0; k < 3 && k < ntile; ++k)
@@ -586,15 +593,8 @@ __global__ void __launch_bounds__(2 * kSplitTeam, 1)
 
     double acc = 0.0;
     for (int k = team; k < ntile; k += 2) {
-        const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[k % 3]));
-        // A parity wait only tells the two newest phases apart: first make
-        // sure this buffer's previous phase (tile k - 3, loaded by this very
-        // team two tiles ago) has completed, then wait for tile k's phase.
-        // Without the first wait a team that computes two tiles faster than
-        // one fill completes reads a half-loaded buffer (seen as a rare wrong
-        // energy on few-group linear passes, 24 qubits / 2000 uniform words).
-        if (k >= 3) mbar_wait(a, static_cast<unsigned>(((k / 3) - 1) & 1));
-        mbar_wait(a, static_cast<unsigned>((k / 3) & 1));
+        const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[fill_bar(k)]));
+        mbar_wait(a, fill_parity(k));
         coset_tile_sets_split(P, bufs + (k % 3) * E, stab, tid, tile_of(k) << kTileBits, pe, acc);
         named_bar(1 + team, kSplitTeam);
         if (k + 3 < ntile) issue(k + 3);

@@ -1,8 +1,8 @@
 #!/bin/bash
 # Round-2 GPU check (run from the repo root under gpurun): full GPU test suite,
 # smoke, then the split-coset EVC A/B.
-O=${OUT:-gpurun_out/r2b}; mkdir -p $O
-timeout 1500 python -m pytest tests -m gpu -q --durations=15 > $O/tests.log 2>&1; echo rc=$? >> $O/tests.log
+O=${OUT:-gpurun_out/r2c}; mkdir -p $O
+timeout 1500 python -m pytest tests -m gpu -q -x --timeout 600 --durations=15 > $O/tests.log 2>&1; echo rc=$? >> $O/tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo rc=$? >> $O/smoke.log
 for sp in 1 0; do
   QRT_EVC_SPLIT=$sp timeout 600 python bench.py --qubits 30 --no-cpu-baseline --steps 2 --warmup 3 > $O/gf30_split$sp.json 2>&1

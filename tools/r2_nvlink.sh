@@ -13,3 +13,16 @@ for ip in 0 1; do
   QRT_QR_INPLACE=$ip BENCH_DEBUG=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29511 \
      bench.py --gpus $N --steps 2 --warmup 3 --no-cpu-baseline > $O/bench32_n${N}_inplace$ip.json 2> $O/bench32_n${N}_inplace$ip.err
 done
+if [ "$N" = "2" ]; then
+  # 34 qubits on 2 GPUs: 128 GiB per GPU, so the QR must run in place (auto)
+  BENCH_DEBUG=1 timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 \
+     bench.py --gpus 2 --qubits 34 --steps 2 --warmup 3 --no-cpu-baseline > $O/bench34_gf_n2.json 2> $O/bench34_gf_n2.err
+fi
+if [ "$N" = "4" ]; then
+  for circ in hea; do
+    BENCH_DEBUG=1 timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29513 \
+       bench.py --gpus 4 --qubits 34 --circuit $circ --steps 2 --warmup 3 --no-cpu-baseline > $O/bench34_${circ}_n4.json 2> $O/bench34_${circ}_n4.err
+  done
+  BENCH_DEBUG=1 timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29514 \
+     bench.py --gpus 4 --qubits 34 --circuit hea --hamiltonian uniform --terms 10000 --steps 1 --warmup 3 --no-cpu-baseline > $O/bench34_c5_n4.json 2> $O/bench34_c5_n4.err
+fi

@@ -153,10 +153,13 @@ int grid_for(std::uint64_t items, int threads, int sms) {
     return static_cast<int>(want < cap ? (want == 0 ? 1 : want) : cap);
 }
 
-// In-place QR policy (QRT_QR_INPLACE: 0 never, 1 always, unset = auto):
-// auto picks it when this process's sub-vectors twice over would not fit in
-// the device memory free now (minus 4 GiB of headroom), e.g. 34 qubits on 2
-// GPUs (2 x 128 GiB per GPU).
+// Single-buffer (in-place QR) policy (QRT_QR_INPLACE: 0 never, 1 always,
+// unset = auto).  The second buffer only serves the fused (pull) QR, which is
+// used up to 2^30 amplitudes per PE; every executed QR runs in place anyway
+// (qrt_reorder.cu execute_qr).  So auto keeps one buffer when the fused QR
+// cannot apply, or when this process's sub-vectors twice over would not fit
+// in the device memory free now (minus 4 GiB of headroom), e.g. 34 qubits on
+// 2 GPUs (2 x 128 GiB per GPU).
 int forced_inplace(int p) {  // -1: automatic
     if (p < 2) return 0;
     const char* e = std::getenv("QRT_QR_INPLACE");
@@ -164,9 +167,10 @@ int forced_inplace(int p) {  // -1: automatic
     return -1;
 }
 
-bool choose_inplace(int p, std::uint64_t state_bytes) {
+bool choose_inplace(int p, int nl, std::uint64_t state_bytes) {
     const int f = forced_inplace(p);
     if (f >= 0) return f != 0;
+    if (!fused_qr_enabled() || nl > fused_qr_max_log2()) return true;
     std::size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
         cudaGetLastError();
@@ -407,7 +411,7 @@ qrt_status qrt_state_create(int n, int p, int device, qrt_comm* comm, qrt_state*
             return;
         }
 
-        const bool inplace = choose_inplace(p, state_bytes);
+        const bool inplace = choose_inplace(p, n - g, state_bytes);
         auto st = new qrt_state;
         st->n = n;
         st->p = p;

@@ -126,6 +126,7 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
 std::uint64_t reorder(qrt_state* st, const int* dest);
 void flush_reorder(qrt_state* st);  // execute a pending QR (no-op if none)
 bool fused_qr_enabled();
+int fused_qr_max_log2();  // largest log2(amplitudes per PE) the fused (pull) QR is used for
 void reorder_plan(int n, int p, const int* dest, int src_pe, std::uint64_t* dst_pe, std::uint64_t* dst_off,
                   std::uint64_t* relocated);
 void qr_bench(int n_gpus, int nl, int k, int inplace, int iters, double* ms_out, double* gbs_out);

@@ -358,6 +358,19 @@ struct InplacePlan {
     std::vector<std::pair<int, int>> cross;  // (local slot, PE bit)
 };
 
+// True when every global position is fed by itself or by a local position
+// (every flat / one-box QR event; hierarchical routing may move a global
+// qubit between the intra and inter regions, which only the push kernel does).
+bool inplace_decomposable(int n, int nl, const int* dest) {
+    std::vector<int> src_of(static_cast<std::size_t>(n), -1);
+    for (int s = 0; s < n; ++s) src_of[static_cast<std::size_t>(dest[s])] = s;
+    for (int t = nl; t < n; ++t) {
+        const int s = src_of[static_cast<std::size_t>(t)];
+        if (s >= nl && s != t) return false;
+    }
+    return true;
+}
+
 InplacePlan plan_inplace(int n, int nl, const int* dest) {
     std::vector<int> src_of(static_cast<std::size_t>(n), -1);
     for (int s = 0; s < n; ++s) src_of[static_cast<std::size_t>(dest[s])] = s;
@@ -474,6 +487,14 @@ void execute_inplace(qrt_state* st, const int* dest, std::uint64_t relocated) {
 }  // namespace
 
 
+int fused_qr_max_log2() {
+    static const int v = [] {
+        const char* e = std::getenv("QRT_FUSED_QR_MAX_LOG2");
+        return e ? std::atoi(e) : 30;
+    }();
+    return v;
+}
+
 bool fused_qr_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("QRT_FUSED_QR");
@@ -515,6 +536,28 @@ void execute_reorder(qrt_state* st, const int* dest) {
     st->cur = nxt;
 }
 
+// An executed (not fused) QR: the in-place pairwise swap whenever the map
+// allows it — it moves only the (1 - 2^-k) that changes PE and measured 679
+// vs 531 GB/s per direction for the push kernel (2 x B200, 2^30 amplitudes
+// per PE, profiles/r2_qr_nvlink.json) — else the push exchange into the spare
+// buffer.  QRT_QR_PUSH=1 forces the push kernel on two-buffer states.
+void execute_qr(qrt_state* st, const int* dest) {
+    static const bool force_push = [] {
+        const char* e = std::getenv("QRT_QR_PUSH");
+        return e && std::atoi(e) != 0;
+    }();
+    const bool decomposable = inplace_decomposable(st->n, st->nl, dest);
+    if (!st->inplace && (force_push || !decomposable)) {
+        execute_reorder(st, dest);
+        return;
+    }
+    if (!decomposable) fail(QRT_ERR_CONFIG, "in-place reorder: global position moves to another global position");
+    QrMap m{};
+    bool identity = false;
+    const std::uint64_t relocated = build_map(st->n, st->nl, st->pe_begin, dest, m, identity);
+    if (!identity) execute_inplace(st, dest, relocated);
+}
+
 }  // namespace
 
 std::uint64_t reorder(qrt_state* st, const int* dest) {
@@ -524,30 +567,26 @@ std::uint64_t reorder(qrt_state* st, const int* dest) {
     if (identity) return 0;
     flush_reorder(st);
     if (st->inplace) {
-        execute_inplace(st, dest, relocated);
+        execute_qr(st, dest);
         return relocated;
     }
     // Pulling a tile's sources over NVLink scatters each CTA's reads over the
     // whole peer buffer; past 2^30 amplitudes (16 GiB) per PE the translation
     // misses outweigh the saved exchange (34-qubit HEA on 4 GPUs: 0.31 s
     // slower), so large states keep the push exchange.
-    static const int max_log2 = [] {
-        const char* e = std::getenv("QRT_FUSED_QR_MAX_LOG2");
-        return e ? std::atoi(e) : 30;
-    }();
-    if (fused_qr_enabled() && st->p > 1 && st->nl <= max_log2) {
+    if (fused_qr_enabled() && st->p > 1 && st->nl <= fused_qr_max_log2()) {
         st->qr_pending = true;  // the next gate pass gathers through it
         st->qr_dest.assign(dest, dest + st->n);
         return relocated;
     }
-    execute_reorder(st, dest);
+    execute_qr(st, dest);
     return relocated;
 }
 
 void flush_reorder(qrt_state* st) {
     if (!st->qr_pending) return;
     st->qr_pending = false;
-    execute_reorder(st, st->qr_dest.data());
+    execute_qr(st, st->qr_dest.data());
 }
 
 void reorder_inplace_plan(int n, int p, const int* dest, int* pairs0, int* n0, int* pairs1, int* n1, int* cross,

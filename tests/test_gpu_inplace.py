@@ -47,8 +47,10 @@ def test_hea_inplace_matches_oracle(qb, device, inplace):
 
 @pytest.mark.parametrize("p", [2, 4])
 def test_inplace_bit_identical_to_push(qb, device, monkeypatch, p):
-    """Same circuit, same schedule: in-place and push QR give identical bits
-    (the QR is a permutation; the gate passes see the same physical layout)."""
+    """Same circuit, same schedule: a single-buffer state (every QR in place)
+    and a two-buffer state (QRs fused into the next gate pass where possible)
+    give identical bits (the QR is a permutation; the gate passes see the
+    same physical layout)."""
     n = 22
     c = qb.gen_gatefabric(n, 2 * n, 1, True)
     d = qb.build_dependency_graph(c)

@@ -112,33 +112,28 @@ __device__ __forceinline__ double coset_group_im(const double2 (&a)[32], const d
 
 // The single-bit groups of mask 1 << K: one_re[K] Re(w)-only, then one_im[K]
 // Im(w)-only (both real, 16-entry tables), then general ones (64 entries).
-// Per-tile group words (group_words below): bits 0-11 the group's sign
-// mask over the thread's tile bits, bit 12 the sign over the tile's outer
-// bits and the PE, bits 16-31 the group's first table double.
-__device__ __forceinline__ int word_odd(unsigned w, int ebase) {
-    return (__popc(static_cast<unsigned>(ebase) & w) ^ static_cast<int>(w >> 12)) & 1;
-}
-__device__ __forceinline__ int word_tab(unsigned w) { return static_cast<int>(w >> 16); }
-
 template <int K>
-__device__ __forceinline__ void coset_ones(const double2 (&a)[32], const CosetSet& S, const double* __restrict__ tabs,
-                                           const unsigned* __restrict__ sgw, int& g, int ebase, double2& acc) {
+__device__ __forceinline__ void coset_ones(const double2 (&a)[32], const CosetParams& P, const CosetSet& S,
+                                           const double* __restrict__ tabs, int& g, std::uint64_t W, std::uint64_t pe,
+                                           double2& acc) {
     const int n = S.one_cnt[K], nre = S.one_re[K], nim = S.one_im[K];
     const double2* __restrict__ t2 = reinterpret_cast<const double2*>(tabs);
     for (int i = 0; i < nre; ++i, ++g) {
-        const unsigned w = sgw[g];
-        const double r = coset_group<1 << K>(a, t2 + (word_tab(w) >> 1));
-        acc.x += word_odd(w, ebase) ? -r : r;
+        const CosetGroup& G = P.groups[g];
+        const double r = coset_group<1 << K>(a, t2 + (G.tab >> 1));
+        const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
+        acc.x += odd ? -r : r;
     }
     for (int i = 0; i < nim; ++i, ++g) {
-        const unsigned w = sgw[g];
-        const double r = coset_group_im<1 << K>(a, t2 + (word_tab(w) >> 1));
-        acc.x += word_odd(w, ebase) ? -r : r;
+        const CosetGroup& G = P.groups[g];
+        const double r = coset_group_im<1 << K>(a, t2 + (G.tab >> 1));
+        const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
+        acc.x += odd ? -r : r;
     }
     for (int i = nre + nim; i < n; ++i, ++g) {
-        const unsigned w = sgw[g];
-        const double2 r = coset_one<1 << K>(a, tabs + word_tab(w), 1);
-        const int odd = word_odd(w, ebase);
+        const CosetGroup& G = P.groups[g];
+        const double2 r = coset_one<1 << K>(a, tabs + G.tab, 1);
+        const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
         acc.x += odd ? -r.x : r.x;
         acc.y += odd ? -r.y : r.y;
     }
@@ -177,27 +172,16 @@ __device__ __noinline__ double2 coset_generic(const double2* __restrict__ tile, 
 // x.  The 15 masks are walked in a fixed unrolled order (one code body per
 // mask, no switch), so the coset stays in registers.
 template <int XQ>
-__device__ __forceinline__ void coset_fast(const double2 (&a)[32], const CosetSet& S, const double2* __restrict__ tabs,
-                                           const unsigned* __restrict__ sgw, unsigned present, int& g, int ebase,
-                                           double2& acc) {
+__device__ __forceinline__ void coset_fast(const double2 (&a)[32], const CosetParams& P, const CosetSet& S,
+                                           const double2* __restrict__ tabs, unsigned present, std::uint64_t W,
+                                           std::uint64_t pe, double2& acc, int& g) {
     if (!((present >> XQ) & 1u)) return;
     const int g1 = S.g_begin + S.xbeg[XQ];  // groups are sorted by mask: this mask's run ends here
     for (; g < g1; ++g) {
-        const unsigned w = sgw[g];
-        const double r = coset_group<XQ>(a, tabs + (word_tab(w) >> 1));
-        acc.x += word_odd(w, ebase) ? -r : r;
-    }
-}
-
-// The pass's group words for one tile (tile index b, PE pe): computed by the
-// team once per tile instead of two 64-bit parities per group and thread.
-__device__ __forceinline__ void group_words(const CosetParams& P, u64 wout, u64 pe, unsigned* __restrict__ sgw,
-                                            int tid, int nthreads) {
-    const int ng = P.n_sets ? P.sets[P.n_sets - 1].g_begin + P.sets[P.n_sets - 1].g_count : 0;
-    for (int g = tid; g < ng; g += nthreads) {
         const CosetGroup& G = P.groups[g];
-        const unsigned hi = static_cast<unsigned>((__popcll(wout & G.mf) + __popcll(pe & G.gz)) & 1);
-        sgw[g] = static_cast<unsigned>(G.mf & 0xFFFull) | (hi << 12) | (static_cast<unsigned>(G.tab) << 16);
+        const double r = coset_group<XQ>(a, tabs + (G.tab >> 1));
+        const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
+        acc.x += odd ? -r : r;
     }
 }
 
@@ -225,8 +209,8 @@ __device__ __forceinline__ double2 block_sum(double2 v, double2* scratch) {
 // the fast (weight-2/4), single-bit and generic groups of the set.
 template <bool GENERIC, bool ONES>
 __device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const double2* __restrict__ tile,
-                                                const double2* __restrict__ stab, const unsigned* __restrict__ sgw,
-                                                int t, double2& acc) {
+                                                const double2* __restrict__ stab, int t, u64 wout, u64 pe,
+                                                double2& acc) {
     for (int s = 0; s < P.n_sets; ++s) {
         const CosetSet& S = P.sets[s];
         int ebase = 0;
@@ -247,37 +231,38 @@ __device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const doub
                 a[r] = tile[o];
             }
         }
+        const u64 W = static_cast<u64>(ebase) | wout;
         const unsigned present = S.present;
-        int g = S.g_begin;
-        coset_fast<3>(a, S, stab, sgw, present, g, ebase, acc);
-        coset_fast<5>(a, S, stab, sgw, present, g, ebase, acc);
-        coset_fast<6>(a, S, stab, sgw, present, g, ebase, acc);
-        coset_fast<9>(a, S, stab, sgw, present, g, ebase, acc);
-        coset_fast<10>(a, S, stab, sgw, present, g, ebase, acc);
-        coset_fast<12>(a, S, stab, sgw, present, g, ebase, acc);
-        coset_fast<15>(a, S, stab, sgw, present, g, ebase, acc);
-        coset_fast<17>(a, S, stab, sgw, present, g, ebase, acc);
-        coset_fast<18>(a, S, stab, sgw, present, g, ebase, acc);
-        coset_fast<20>(a, S, stab, sgw, present, g, ebase, acc);
-        coset_fast<23>(a, S, stab, sgw, present, g, ebase, acc);
-        coset_fast<24>(a, S, stab, sgw, present, g, ebase, acc);
-        coset_fast<27>(a, S, stab, sgw, present, g, ebase, acc);
-        coset_fast<29>(a, S, stab, sgw, present, g, ebase, acc);
-        coset_fast<30>(a, S, stab, sgw, present, g, ebase, acc);
+        int gf = S.g_begin;
+        coset_fast<3>(a, P, S, stab, present, W, pe, acc, gf);
+        coset_fast<5>(a, P, S, stab, present, W, pe, acc, gf);
+        coset_fast<6>(a, P, S, stab, present, W, pe, acc, gf);
+        coset_fast<9>(a, P, S, stab, present, W, pe, acc, gf);
+        coset_fast<10>(a, P, S, stab, present, W, pe, acc, gf);
+        coset_fast<12>(a, P, S, stab, present, W, pe, acc, gf);
+        coset_fast<15>(a, P, S, stab, present, W, pe, acc, gf);
+        coset_fast<17>(a, P, S, stab, present, W, pe, acc, gf);
+        coset_fast<18>(a, P, S, stab, present, W, pe, acc, gf);
+        coset_fast<20>(a, P, S, stab, present, W, pe, acc, gf);
+        coset_fast<23>(a, P, S, stab, present, W, pe, acc, gf);
+        coset_fast<24>(a, P, S, stab, present, W, pe, acc, gf);
+        coset_fast<27>(a, P, S, stab, present, W, pe, acc, gf);
+        coset_fast<29>(a, P, S, stab, present, W, pe, acc, gf);
+        coset_fast<30>(a, P, S, stab, present, W, pe, acc, gf);
         int g1 = S.g_begin + S.xbeg[31];
         if (ONES) {
             const double* __restrict__ dt = reinterpret_cast<const double*>(stab);
-            coset_ones<0>(a, S, dt, sgw, g1, ebase, acc);
-            coset_ones<1>(a, S, dt, sgw, g1, ebase, acc);
-            coset_ones<2>(a, S, dt, sgw, g1, ebase, acc);
-            coset_ones<3>(a, S, dt, sgw, g1, ebase, acc);
-            coset_ones<4>(a, S, dt, sgw, g1, ebase, acc);
+            coset_ones<0>(a, P, S, dt, g1, W, pe, acc);
+            coset_ones<1>(a, P, S, dt, g1, W, pe, acc);
+            coset_ones<2>(a, P, S, dt, g1, W, pe, acc);
+            coset_ones<3>(a, P, S, dt, g1, W, pe, acc);
+            coset_ones<4>(a, P, S, dt, g1, W, pe, acc);
         }
         if (GENERIC)
-        for (int gg = g1; gg < S.g_begin + S.g_count; ++gg) {
-            const CosetGroup& G = P.groups[gg];
+        for (int g = g1; g < S.g_begin + S.g_count; ++g) {
+            const CosetGroup& G = P.groups[g];
             const double2 r = coset_generic(tile, sb, swq, G.xq, G.mode, P.tabs + G.tab);
-            const int odd = word_odd(sgw[gg], ebase);
+            const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
             acc.x += odd ? -r.x : r.x;
             acc.y += odd ? -r.y : r.y;
         }
@@ -290,7 +275,6 @@ __global__ void __launch_bounds__(kCosetThreads, MINB)
                       double* __restrict__ red) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double2 scratch[kCosetThreads / 32];
-    __shared__ unsigned sgw[kCosetMaxGroups];
     constexpr int E = 1 << kTileBits;
     const int c = P.c, t = threadIdx.x;
     double2* tile = reinterpret_cast<double2*>(smem_raw);
@@ -320,7 +304,6 @@ __global__ void __launch_bounds__(kCosetThreads, MINB)
         const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&tile[swz(e)]));
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(&v[base ^ tabo[e >> c] ^ (e & cmask)]));
     }
-    group_words(P, b << kTileBits, pe, sgw, t, kCosetThreads);
     asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
 
@@ -349,7 +332,7 @@ __global__ void __launch_bounds__(kCosetThreads, MINB)
         }
     }
 
-    coset_tile_sets<GENERIC, ONES>(P, tile, stab, sgw, t, acc);
+    coset_tile_sets<GENERIC, ONES>(P, tile, stab, t, b << kTileBits, pe, acc);
     const double2 tot = block_sum(acc, scratch);
     if (t == 0) {
         double* slot = red + 2 * (static_cast<std::size_t>(blockIdx.y) * gridDim.x + blockIdx.x);
@@ -399,11 +382,9 @@ __global__ void __launch_bounds__(2 * kCosetThreads, 1)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double2 scratch[2 * kCosetThreads / 32];
     __shared__ __align__(8) unsigned long long full[6];
-    __shared__ unsigned sgw_all[2][kCosetMaxGroups];  // per-team group words of its current tile
     constexpr int E = 1 << kTileBits;
     const int c = P.c;
     const int team = threadIdx.x >> 7, tid = threadIdx.x & (kCosetThreads - 1);
-    unsigned* __restrict__ sgw = sgw_all[team];
     double2* bufs = reinterpret_cast<double2*>(smem_raw);  // 3 x E
     u64* tabo = reinterpret_cast<u64*>(bufs + 3 * E);
     double2* stab = reinterpret_cast<double2*>(tabo + ((1 << (kTileBits - c)) | 1) + 1);
@@ -433,21 +414,25 @@ __global__ void __launch_bounds__(2 * kCosetThreads, 1)
     auto tile_of = [&](int k) { return static_cast<u64>(blockIdx.x) + static_cast<u64>(k) * stride; };
     auto issue = [&](int k) {  // this team's 128 threads fill buffer k % 3 with tile k
         const u64 b = tile_of(k);
+        // base = XOR of the outer axes of b's set bits: lane i takes axes i, i+32, ...
+        // and the warp XOR-reduces (instead of every thread walking all axes)
         u64 base = 0;
-        for (int i = 0; i < P.n_outer; ++i)
+        for (int i = tid & 31; i < P.n_outer; i += 32)
             if ((b >> i) & 1ull) base ^= P.outer_vec[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) base ^= __shfl_xor_sync(0xffffffffu, base, o);
         double2* tile = bufs + (k % 3) * E;
         if (c <= 7) {
             // e = tid + 128 i: the swizzle is GF(2)-linear, so swz(e) = swz(tid) ^ swz(128 i)
             // (a constant per unrolled i), and e >> c / e & cmask split the same way
             const unsigned sa0 = static_cast<unsigned>(__cvta_generic_to_shared(tile));
             const int tsw = swz(tid), th = tid >> c;
-            const amp_t* __restrict__ vb = v + (base ^ (tid & cmask));
+            const u64 bl = base ^ static_cast<u64>(tid & cmask);
 #pragma unroll 8
             for (int i = 0; i < E / kCosetThreads; ++i) {
                 const unsigned sa = sa0 + 16u * static_cast<unsigned>(tsw ^ swz(i * kCosetThreads));
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
-                             "l"(vb + tabo[th + (i << (7 - c))]));
+                             "l"(v + (bl ^ tabo[th + (i << (7 - c))])));
             }
         } else {
             for (int e = tid; e < E; e += kCosetThreads) {
@@ -466,10 +451,8 @@ __global__ void __launch_bounds__(2 * kCosetThreads, 1)
     double2 acc = make_double2(0.0, 0.0);
     for (int k = team; k < ntile; k += 2) {
         const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[fill_bar(k)]));
-        group_words(P, tile_of(k) << kTileBits, pe, sgw, tid, kCosetThreads);
-        named_bar(1 + team, kCosetThreads);  // the team's group words are in place
         mbar_wait(a, fill_parity(k));
-        coset_tile_sets<GENERIC, ONES>(P, bufs + (k % 3) * E, stab, sgw, tid, acc);
+        coset_tile_sets<GENERIC, ONES>(P, bufs + (k % 3) * E, stab, tid, tile_of(k) << kTileBits, pe, acc);
         named_bar(1 + team, kCosetThreads);  // the team is done reading buffer k % 3
         if (k + 3 < ntile) issue(k + 3);
     }

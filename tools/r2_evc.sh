@@ -1,7 +1,7 @@
 #!/bin/bash
 # EVC kernel iteration: GPU EVC tests, 30q GF/HEA bench lines, uniform 30q, ncu of the pipe kernel
 O=${OUT:-gpurun_out/r2evc}; mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_evc.py tests/test_gpu_configs.py tests/test_gpu_abi.py -q -x --timeout 300 > $O/tests.log 2>&1; echo rc=$? >> $O/tests.log
+timeout 1500 python -m pytest tests -m gpu -q -x --timeout 600 > $O/tests.log 2>&1; echo rc=$? >> $O/tests.log
 timeout 600 python bench.py --qubits 30 --no-cpu-baseline --steps 2 --warmup 3 > $O/gf30.json 2>&1
 timeout 600 python bench.py --qubits 30 --circuit hea --no-cpu-baseline --steps 2 --warmup 3 > $O/hea30.json 2>&1
 timeout 600 python bench.py --qubits 30 --circuit hea --hamiltonian uniform --terms 1000 --no-cpu-baseline --steps 2 --warmup 3 > $O/hea30_uni1000.json 2>&1

@@ -422,13 +422,13 @@ __global__ void __launch_bounds__(2 * kCosetThreads, 1)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) base ^= __shfl_xor_sync(0xffffffffu, base, o);
         double2* tile = bufs + (k % 3) * E;
-        if (c <= 7) {
+        if (c <= 7 && P.fill_mode) {
             // e = tid + 128 i: the swizzle is GF(2)-linear, so swz(e) = swz(tid) ^ swz(128 i)
             // (a constant per unrolled i), and e >> c / e & cmask split the same way
             const unsigned sa0 = static_cast<unsigned>(__cvta_generic_to_shared(tile));
             const int tsw = swz(tid), th = tid >> c;
             const u64 bl = base ^ static_cast<u64>(tid & cmask);
-#pragma unroll 8
+#pragma unroll
             for (int i = 0; i < E / kCosetThreads; ++i) {
                 const unsigned sa = sa0 + 16u * static_cast<unsigned>(tsw ^ swz(i * kCosetThreads));
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
@@ -630,8 +630,13 @@ __global__ void __launch_bounds__(2 * kSplitTeam, 1)
 
 }  // namespace
 
-void launch_coset_pass(const CosetParams& P, const CosetDiagTerm* dterms, int pe_count, double* red,
+void launch_coset_pass(CosetParams& P, const CosetDiagTerm* dterms, int pe_count, double* red,
                        cudaStream_t stream, int device) {
+    static const int fill_mode = [] {
+        const char* e = std::getenv("QRT_EVC_FILL");
+        return e ? std::atoi(e) : 1;
+    }();
+    P.fill_mode = fill_mode;
     // Launches holding only Jordan-Wigner-type groups take the fast-only
     // kernel (218 registers, 2 CTAs/SM; QRT_COSET_OCC=3 squeezes it to 3 CTAs/SM
     // with spills, measured slower); any generic group needs the

@@ -174,10 +174,10 @@ __device__ __noinline__ double2 coset_generic(const double2* __restrict__ tile, 
 template <int XQ>
 __device__ __forceinline__ void coset_fast(const double2 (&a)[32], const CosetParams& P, const CosetSet& S,
                                            const double2* __restrict__ tabs, unsigned present, std::uint64_t W,
-                                           std::uint64_t pe, double2& acc, int& g) {
+                                           std::uint64_t pe, double2& acc) {
     if (!((present >> XQ) & 1u)) return;
-    const int g1 = S.g_begin + S.xbeg[XQ];  // groups are sorted by mask: this mask's run ends here
-    for (; g < g1; ++g) {
+    const int g0 = S.g_begin + S.xbeg[XQ - 1], g1 = S.g_begin + S.xbeg[XQ];
+    for (int g = g0; g < g1; ++g) {
         const CosetGroup& G = P.groups[g];
         const double r = coset_group<XQ>(a, tabs + (G.tab >> 1));
         const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
@@ -233,22 +233,21 @@ __device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const doub
         }
         const u64 W = static_cast<u64>(ebase) | wout;
         const unsigned present = S.present;
-        int gf = S.g_begin;
-        coset_fast<3>(a, P, S, stab, present, W, pe, acc, gf);
-        coset_fast<5>(a, P, S, stab, present, W, pe, acc, gf);
-        coset_fast<6>(a, P, S, stab, present, W, pe, acc, gf);
-        coset_fast<9>(a, P, S, stab, present, W, pe, acc, gf);
-        coset_fast<10>(a, P, S, stab, present, W, pe, acc, gf);
-        coset_fast<12>(a, P, S, stab, present, W, pe, acc, gf);
-        coset_fast<15>(a, P, S, stab, present, W, pe, acc, gf);
-        coset_fast<17>(a, P, S, stab, present, W, pe, acc, gf);
-        coset_fast<18>(a, P, S, stab, present, W, pe, acc, gf);
-        coset_fast<20>(a, P, S, stab, present, W, pe, acc, gf);
-        coset_fast<23>(a, P, S, stab, present, W, pe, acc, gf);
-        coset_fast<24>(a, P, S, stab, present, W, pe, acc, gf);
-        coset_fast<27>(a, P, S, stab, present, W, pe, acc, gf);
-        coset_fast<29>(a, P, S, stab, present, W, pe, acc, gf);
-        coset_fast<30>(a, P, S, stab, present, W, pe, acc, gf);
+        coset_fast<3>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<5>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<6>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<9>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<10>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<12>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<15>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<17>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<18>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<20>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<23>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<24>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<27>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<29>(a, P, S, stab, present, W, pe, acc);
+        coset_fast<30>(a, P, S, stab, present, W, pe, acc);
         int g1 = S.g_begin + S.xbeg[31];
         if (ONES) {
             const double* __restrict__ dt = reinterpret_cast<const double*>(stab);
@@ -414,32 +413,14 @@ __global__ void __launch_bounds__(2 * kCosetThreads, 1)
     auto tile_of = [&](int k) { return static_cast<u64>(blockIdx.x) + static_cast<u64>(k) * stride; };
     auto issue = [&](int k) {  // this team's 128 threads fill buffer k % 3 with tile k
         const u64 b = tile_of(k);
-        // base = XOR of the outer axes of b's set bits: lane i takes axes i, i+32, ...
-        // and the warp XOR-reduces (instead of every thread walking all axes)
         u64 base = 0;
-        for (int i = tid & 31; i < P.n_outer; i += 32)
+        for (int i = 0; i < P.n_outer; ++i)
             if ((b >> i) & 1ull) base ^= P.outer_vec[i];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) base ^= __shfl_xor_sync(0xffffffffu, base, o);
         double2* tile = bufs + (k % 3) * E;
-        if (c <= 7 && P.fill_mode) {
-            // e = tid + 128 i: the swizzle is GF(2)-linear, so swz(e) = swz(tid) ^ swz(128 i)
-            // (a constant per unrolled i), and e >> c / e & cmask split the same way
-            const unsigned sa0 = static_cast<unsigned>(__cvta_generic_to_shared(tile));
-            const int tsw = swz(tid), th = tid >> c;
-            const u64 bl = base ^ static_cast<u64>(tid & cmask);
-#pragma unroll
-            for (int i = 0; i < E / kCosetThreads; ++i) {
-                const unsigned sa = sa0 + 16u * static_cast<unsigned>(tsw ^ swz(i * kCosetThreads));
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
-                             "l"(v + (bl ^ tabo[th + (i << (7 - c))])));
-            }
-        } else {
-            for (int e = tid; e < E; e += kCosetThreads) {
-                const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&tile[swz(e)]));
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
-                             "l"(&v[base ^ tabo[e >> c] ^ (e & cmask)]));
-            }
+        for (int e = tid; e < E; e += kCosetThreads) {
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&tile[swz(e)]));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
+                         "l"(&v[base ^ tabo[e >> c] ^ (e & cmask)]));
         }
         const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[fill_bar(k)]));
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a));
@@ -630,13 +611,8 @@ __global__ void __launch_bounds__(2 * kSplitTeam, 1)
 
 }  // namespace
 
-void launch_coset_pass(CosetParams& P, const CosetDiagTerm* dterms, int pe_count, double* red,
+void launch_coset_pass(const CosetParams& P, const CosetDiagTerm* dterms, int pe_count, double* red,
                        cudaStream_t stream, int device) {
-    static const int fill_mode = [] {
-        const char* e = std::getenv("QRT_EVC_FILL");
-        return e ? std::atoi(e) : 1;
-    }();
-    P.fill_mode = fill_mode;
     // Launches holding only Jordan-Wigner-type groups take the fast-only
     // kernel (218 registers, 2 CTAs/SM; QRT_COSET_OCC=3 squeezes it to 3 CTAs/SM
     // with spills, measured slower); any generic group needs the

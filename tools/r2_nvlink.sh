@@ -19,6 +19,10 @@ if [ "$N" = "2" ]; then
      bench.py --gpus 2 --qubits 34 --steps 2 --warmup 3 --no-cpu-baseline > $O/bench34_gf_n2.json 2> $O/bench34_gf_n2.err
 fi
 if [ "$N" = "4" ]; then
+  for circ in gatefabric hea; do
+    timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29515 \
+       bench.py --gpus 4 --qubits 30 --circuit $circ --steps 2 --warmup 3 --no-cpu-baseline > $O/bench30_${circ}_n4.json 2> $O/bench30_${circ}_n4.err
+  done
   for circ in hea; do
     BENCH_DEBUG=1 timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29513 \
        bench.py --gpus 4 --qubits 34 --circuit $circ --steps 2 --warmup 3 --no-cpu-baseline > $O/bench34_${circ}_n4.json 2> $O/bench34_${circ}_n4.err

@@ -1,8 +1,9 @@
 #!/bin/bash
 # N-GPU NVLink QR evidence (single process): event-timed rates, then ncu NVLink counters.
-O=${OUT:-gpurun_out/r2nvl}; mkdir -p $O
+O=${OUT:-gpurun_out/r2nvl$(nvidia-smi -L | wc -l)}; mkdir -p $O
 N=$(nvidia-smi -L | wc -l)
 nvidia-smi topo -m > $O/topo.txt 2>&1
+[ -x tools/mb_imma ] && timeout 120 tools/mb_imma > $O/mb_imma.txt 2>&1
 timeout 600 python tools/qr_nvlink.py --nl 30 --iters 5 > $O/qr_nl30_n$N.jsonl 2> $O/qr.err
 timeout 600 python tools/qr_nvlink.py --nl 31 --iters 3 > $O/qr_nl31_n$N.jsonl 2>> $O/qr.err
 timeout 900 ncu --clock-control none --metrics gpu__time_duration.sum,nvltx__bytes.sum,nvlrx__bytes.sum,nvltx__bytes_data_user.sum,nvlrx__bytes_data_user.sum,dram__bytes_read.sum,dram__bytes_write.sum \

@@ -52,6 +52,9 @@ typedef struct qrt_state qrt_state; /* distributed state: buffers, streams   */
 /* Message of the last failing call on this thread ("" if none). */
 const char* qrt_last_error(void);
 int qrt_abi_version(void);
+/* Build flags: bit 0 = checked build (libqrt_checked.so: device-side bounds
+ * and pipeline invariant checks, QRT_CHECKS). */
+int qrt_build_flags(void);
 /* Number of visible CUDA devices of compute capability 10.x. */
 qrt_status qrt_device_count(int* out);
 

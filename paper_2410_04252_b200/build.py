@@ -31,6 +31,8 @@ HOST_SRCS = ["qubit_core.cpp", "relayout.cpp", "tiling_qsu.cpp", "tiling_evc.cpp
              "device_state.cpp"]
 
 LIBQRT = PKG / "libqrt.so"
+LIBQRT_CHECKED = PKG / "libqrt_checked.so"
+BUILD_CHECKED = PKG / "_build_checked"
 LIBHOST = PKG / "libqrtile_b200.so"
 EXT = PKG / ("_qrtile" + sysconfig.get_config_var("EXT_SUFFIX"))
 
@@ -54,24 +56,29 @@ def _headers() -> list[Path]:
             + list((PKG / "host" / "include" / "qrtile").glob("*.hpp")))
 
 
-def build_libqrt() -> Path:
-    BUILD.mkdir(exist_ok=True)
+def build_libqrt(checked: bool = False) -> Path:
+    """libqrt.so, or with checked=True libqrt_checked.so: the same kernels with
+    -DQRT_CHECKS device-side bounds / pipeline checks (tests preload it)."""
+    bdir = BUILD_CHECKED if checked else BUILD
+    out = LIBQRT_CHECKED if checked else LIBQRT
+    bdir.mkdir(exist_ok=True)
     objs, jobs = [], []
     for src in CU_SRCS:
         s = PKG / "csrc" / src
-        o = BUILD / (src + ".o")
+        o = bdir / (src + ".o")
         objs.append(o)
         if _stale(o, [s] + _headers()):
             jobs.append([NVCC, "-std=c++17", *ARCH, "-O3", "-lineinfo", "-Xcompiler", "-fPIC",
+                         *(["-DQRT_CHECKS"] if checked else []),
                          "-I", str(ROOT / "include"), "-I", str(NCCL / "include"),
                          "-c", str(s), "-o", str(o)])
     with ThreadPoolExecutor(max_workers=4) as ex:
         list(ex.map(_run, jobs))
-    if _stale(LIBQRT, objs):
-        _run([NVCC, "-shared", *ARCH, "-o", str(LIBQRT), *map(str, objs),
+    if _stale(out, objs):
+        _run([NVCC, "-shared", *ARCH, "-o", str(out), *map(str, objs),
               "-L", str(NCCL / "lib"), "-l:libnccl.so.2",
               "-Xlinker", "-rpath," + str(NCCL / "lib")])
-    return LIBQRT
+    return out
 
 
 def build_host() -> Path:
@@ -111,6 +118,7 @@ def build_oracle() -> None:
 def build() -> None:
     build_libqrt()
     build_host()
+    build_libqrt(checked=True)
     build_oracle()
 
 

@@ -268,6 +268,7 @@ extern "C" {
 
 const char* qrt_last_error(void) { return g_last_error.c_str(); }
 int qrt_abi_version(void) { return QRT_ABI_VERSION; }
+int qrt_build_flags(void) { return kBuildFlags; }
 
 qrt_status qrt_device_count(int* out) {
     return guarded([&] {

@@ -301,6 +301,7 @@ __global__ void __launch_bounds__(kCosetThreads, MINB)
     const int cmask = (1 << c) - 1;
     for (int e = t; e < E; e += kCosetThreads) {
         const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&tile[swz(e)]));
+        QRT_DCHECK((base ^ tabo[e >> c] ^ (e & cmask)) < (static_cast<u64>(P.tiles_per_pe) << kTileBits));
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(&v[base ^ tabo[e >> c] ^ (e & cmask)]));
     }
     asm volatile("cp.async.wait_all;\n" ::);
@@ -419,6 +420,7 @@ __global__ void __launch_bounds__(2 * kCosetThreads, 1)
         double2* tile = bufs + (k % 3) * E;
         for (int e = tid; e < E; e += kCosetThreads) {
             const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&tile[swz(e)]));
+            QRT_DCHECK((base ^ tabo[e >> c] ^ (e & cmask)) < (static_cast<u64>(P.tiles_per_pe) << kTileBits));
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
                          "l"(&v[base ^ tabo[e >> c] ^ (e & cmask)]));
         }
@@ -433,6 +435,20 @@ __global__ void __launch_bounds__(2 * kCosetThreads, 1)
     for (int k = team; k < ntile; k += 2) {
         const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[fill_bar(k)]));
         mbar_wait(a, fill_parity(k));
+        QRT_DCHECK((k & 1) == team && k < ntile);
+#ifdef QRT_CHECKS
+        {  // the awaited buffer really holds tile k (the state is read-only during EVC)
+            const u64 bk = tile_of(k);
+            u64 base = 0;
+            for (int i = 0; i < P.n_outer; ++i)
+                if ((bk >> i) & 1ull) base ^= P.outer_vec[i];
+            for (int e = tid; e < E; e += 16 * kCosetThreads) {
+                const double2 want = v[base ^ tabo[e >> c] ^ (e & cmask)];
+                const double2 got = bufs[(k % 3) * E + swz(e)];
+                QRT_DCHECK(got.x == want.x && got.y == want.y);
+            }
+        }
+#endif
         coset_tile_sets<GENERIC, ONES>(P, bufs + (k % 3) * E, stab, tid, tile_of(k) << kTileBits, pe, acc);
         named_bar(1 + team, kCosetThreads);  // the team is done reading buffer k % 3
         if (k + 3 < ntile) issue(k + 3);
@@ -582,6 +598,7 @@ __global__ void __launch_bounds__(2 * kSplitTeam, 1)
         double2* tile = bufs + (k % 3) * E;
         for (int e = tid; e < E; e += kSplitTeam) {
             const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&tile[swz(e)]));
+            QRT_DCHECK((base ^ tabo[e >> c] ^ (e & cmask)) < (static_cast<u64>(P.tiles_per_pe) << kTileBits));
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
                          "l"(&v[base ^ tabo[e >> c] ^ (e & cmask)]));
         }

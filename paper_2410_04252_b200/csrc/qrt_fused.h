@@ -60,6 +60,7 @@ __device__ __forceinline__ const amp_t* fused_src(const FusedSource& f, const st
     const std::uint64_t* hi = words + kFusedSmemWords;
     const int el = e & cmask;
     const std::uint64_t S = words[128] ^ hi[e >> c] ^ words[el & 63] ^ words[64 + ((el >> 6) & 63)];
+    QRT_DCHECK((S >> f.nl) < (1ull << (f.n - f.nl)) && f.src[S >> f.nl] != nullptr);
     return f.src[S >> f.nl] + (S & ((1ull << f.nl) - 1));
 }
 

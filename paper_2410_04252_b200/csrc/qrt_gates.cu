@@ -478,7 +478,10 @@ __global__ void __launch_bounds__(128, MINB)
         for (int e = threadIdx.x; e < E; e += blockDim.x) cp_async16(&tile[swz(e)], fused_src(*fs, words, e, cmask, c));
         v = fs->dst[t / tiles_per_pe];
     } else {
-        for (int e = threadIdx.x; e < E; e += blockDim.x) cp_async16(&tile[swz(e)], &v[base | tab[e >> c] | (e & cmask)]);
+        for (int e = threadIdx.x; e < E; e += blockDim.x) {
+            QRT_DCHECK((base | tab[e >> c] | (e & cmask)) < (static_cast<std::uint64_t>(tiles_per_pe) << T));
+            cp_async16(&tile[swz(e)], &v[base | tab[e >> c] | (e & cmask)]);
+        }
     }
     cp_async_wait_all();
     __syncthreads();
@@ -519,7 +522,10 @@ __global__ void __launch_bounds__(128, MINB)
         }
         __syncthreads();
     }
-    for (int e = threadIdx.x; e < E; e += blockDim.x) __stcs(&v[base | tab[e >> c] | (e & cmask)], tile[swz(e)]);
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        QRT_DCHECK((base | tab[e >> c] | (e & cmask)) < (static_cast<std::uint64_t>(tiles_per_pe) << T));
+        __stcs(&v[base | tab[e >> c] | (e & cmask)], tile[swz(e)]);
+    }
 }
 
 // Out-of-place generic gate for very wide payloads: out[i] = sum_c U[row(i)][c] in[...].

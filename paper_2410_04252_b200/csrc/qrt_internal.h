@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -27,6 +28,25 @@ void nccl_check(ncclResult_t r, const char* what, const char* file, int line);
 #define QRT_NCCL(x) ::qrt::nccl_check((x), #x, __FILE__, __LINE__)
 
 using amp_t = double2;  // (re, im), 16 B, the HBM unit
+
+// Checked build (libqrt_checked.so, -DQRT_CHECKS): device-side bounds and
+// invariant checks in the kernels; a failure prints the condition and traps
+// (the call then fails with QRT_ERR_CUDA).  compute-sanitizer is closed on
+// the GPU pool, so tests run the small parity cases through this build.
+#ifdef QRT_CHECKS
+#define QRT_DCHECK(cond)                                                                        \
+    do {                                                                                        \
+        if (!(cond)) {                                                                          \
+            printf("QRT_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+                   static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+inline constexpr int kBuildFlags = 1;
+#else
+#define QRT_DCHECK(cond) ((void)0)
+inline constexpr int kBuildFlags = 0;
+#endif
 
 inline constexpr int kMaxLocalPEs = 64;  // PEs one process may own
 inline constexpr int kTileBits = 12;     // smem tile: 2^12 amplitudes = 64 KiB

@@ -99,8 +99,11 @@ __global__ void __launch_bounds__(256) reorder_kernel(const __grid_constant__ Qr
     for (int cls = 0; cls < ncls; ++cls) {
         const Bases b = qr_bases(a.m, j, chunk, cls);
         amp_t* __restrict__ dst = a.dst[b.pe];
-        for (int e = threadIdx.x; e < E; e += blockDim.x)
+        QRT_DCHECK(b.pe >= 0 && b.pe < (1 << a.m.g) && dst != nullptr);
+        for (int e = threadIdx.x; e < E; e += blockDim.x) {
+            QRT_DCHECK((b.dst | qr_dst_e(a.m, e)) < (1ull << a.m.nl) && (b.src | qr_src_e(a.m, e)) < (1ull << a.m.nl));
             dst[b.dst | qr_dst_e(a.m, e)] = __ldcs(&src[b.src | qr_src_e(a.m, e)]);
+        }
     }
     __threadfence_system();  // peer stores visible before the stream-ordered barrier
 }
@@ -235,6 +238,7 @@ struct XchgArgs {
     int d_pos[8];   // local slot of transposition i
     int pe_bit[8];  // PE-index bit of transposition i
     int f;          // free local position splitting each class pair between its two PEs (-1: none)
+    int nl, p;      // local positions, PEs (QRT_CHECKS bounds)
     Deposit dep;    // the remaining local positions
 };
 
@@ -271,6 +275,7 @@ __global__ void __launch_bounds__(256) exchange_kernel(const __grid_constant__ X
         ob |= hi;
         pb |= hi;
         amp_t* __restrict__ peer = a.pe_ptr[sp];
+        QRT_DCHECK(sp >= 0 && sp < a.p && sp != j && peer != nullptr);
         for (int e0 = threadIdx.x; e0 < E; e0 += kXchgUnroll * blockDim.x) {
             amp_t x[kXchgUnroll], y[kXchgUnroll];
             std::uint64_t lo[kXchgUnroll];
@@ -279,6 +284,7 @@ __global__ void __launch_bounds__(256) exchange_kernel(const __grid_constant__ X
                 const int e = e0 + u * static_cast<int>(blockDim.x);
                 lo[u] = e < E ? dep_lo(a.dep, e) : 0;
                 if (e < E) {
+                    QRT_DCHECK((ob | lo[u]) < (1ull << a.nl) && (pb | lo[u]) < (1ull << a.nl) && ob != pb);
                     x[u] = __ldcs(&mine[ob | lo[u]]);
                     y[u] = __ldcs(&peer[pb | lo[u]]);
                 }
@@ -301,6 +307,7 @@ struct LocalSwapArgs {
     int m;                     // disjoint transpositions (a_i <-> c_i), a_i < c_i
     int a_pos[8];
     int c_pos[8];
+    int nl;                    // local positions (QRT_CHECKS bounds)
     Deposit dep;               // the other local positions
 };
 
@@ -333,6 +340,7 @@ __global__ void __launch_bounds__(256) local_swap_kernel(const __grid_constant__
                 const int e = e0 + u * static_cast<int>(blockDim.x);
                 lo[u] = e < E ? dep_lo(a.dep, e) : 0;
                 if (e < E) {
+                    QRT_DCHECK((pb | lo[u]) < (1ull << a.nl) && (ob | lo[u]) < (pb | lo[u]));
                     x[u] = __ldcs(&v[ob | lo[u]]);
                     y[u] = __ldcs(&v[pb | lo[u]]);
                 }
@@ -430,6 +438,7 @@ void launch_local_swaps(qrt_state* st, const std::vector<std::pair<int, int>>& p
         for (int x = 0; x < st->nl; ++x)
             if (!used[static_cast<std::size_t>(x)]) rest.push_back(x);
         make_deposit(rest, a.dep);
+        a.nl = st->nl;
         for (int i = 0; i < st->pe_count; ++i) a.ptr[i] = st->live(i);
         const std::uint64_t work = (1ull << (2 * a.m)) << a.dep.n_hi;
         const unsigned gx = static_cast<unsigned>(std::min<std::uint64_t>(work, static_cast<std::uint64_t>(st->sm_count) * 8));
@@ -467,6 +476,8 @@ void execute_inplace(qrt_state* st, const int* dest, std::uint64_t relocated) {
     for (int x = 0; x < st->nl; ++x)
         if (!used[static_cast<std::size_t>(x)]) rest.push_back(x);
     make_deposit(rest, a.dep);
+    a.nl = st->nl;
+    a.p = st->p;
     for (int pe = 0; pe < st->p; ++pe) a.pe_ptr[pe] = st->peer[st->cur][static_cast<std::size_t>(pe)];
     barrier_on_stream(st);  // every peer is done with the buffers touched here
     {
@@ -697,6 +708,8 @@ void qr_bench(int n_gpus, int nl, int k, int inplace, int iters, double* ms_out,
             for (int x = 0; x < nl; ++x)
                 if (!used[static_cast<std::size_t>(x)]) rest.push_back(x);
             make_deposit(rest, a.dep);
+            a.nl = nl;
+            a.p = n_gpus;
             for (int pe = 0; pe < n_gpus; ++pe) a.pe_ptr[pe] = b0[static_cast<std::size_t>(pe)];
         }
         double total_ms = 0.0;

@@ -373,4 +373,5 @@ PYBIND11_MODULE(_qrtile, m) {
     });
     m.attr("kOracleMaxQubits") = kOracleMaxQubits;
     m.attr("QRT_ABI_VERSION") = QRT_ABI_VERSION;
+    m.def("build_flags", []() { return qrt_build_flags(); });
 }

@@ -255,7 +255,11 @@ __global__ void __launch_bounds__(256) exchange_kernel(const __grid_constant__ X
     for (std::uint64_t w = blockIdx.x; w < work; w += gridDim.x) {
         const int ci = static_cast<int>(w / chunks);
         const std::uint64_t chunk = w % chunks;
-        const int s = ci >= jc ? ci + 1 : ci;  // the partner's class (never jc: that class stays)
+        // XOR schedule: at step ci every PE j works with the PE whose class
+        // bits are jc ^ (ci + 1), a perfect matching, so all GPUs exchange
+        // pairwise at once instead of converging on one partner (an in-cast
+        // that held k = 2 on 4 GPUs at 440 GB/s); never jc, which stays
+        const int s = jc ^ (ci + 1);
         int sp = j;
         std::uint64_t ob = 0, pb = 0;
         for (int i = 0; i < a.k; ++i) {

@@ -333,8 +333,11 @@ def cmd_simulate(cfg, out, diag):
         report["verify"] = {"max_amp_error": worst, "pass": ok}
         code = 0 if ok else 1
     if cfg.out:
-        with open(cfg.out, "wb") as f:
-            f.write(qb.write_state_dump(final, shape.p))
+        try:
+            with open(cfg.out, "wb") as f:
+                f.write(qb.write_state_dump(final, shape.p))
+        except OSError:  # report.cpp:184-185: ConfigError, exit code 2
+            raise qb.ConfigError(f"cannot write output file: {cfg.out}") from None
         report["dump"] = cfg.out
     out.write(_dumps(report))
     if code:

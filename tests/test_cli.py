@@ -174,3 +174,10 @@ def test_evc_diagonalize_tiles_and_circuit(qb, device, tmp_path):  # :153-166 + 
     circ = write(tmp_path, "gf8.qct", cli.serialize_circuit(qb.gen_gatefabric(8, 6, 1, False)))
     code, out, _ = run(f"evc --hamiltonian {ham} --circuit {circ} --p 2 --verify --seed 3")
     assert code == 0 and json.loads(out)["verify"]["pass"]
+
+
+@pytest.mark.gpu
+def test_simulate_unwritable_dump_exit_2(qb, device, tmp_path):  # report.cpp:184-185
+    path = write(tmp_path, "empty.qct", "n 4\n")
+    code, _, err = run(f"simulate --circuit {path} --p 2 --out {tmp_path}/no/such/dir/x.bin")
+    assert code == 2 and "cannot write output file" in err

@@ -557,6 +557,76 @@ __global__ void wide_gate_kernel(const amp_t* __restrict__ in, amp_t* __restrict
     }
 }
 
+// In-place generic gate for 8 <= k <= kWideInPlaceK dense qubits: one CTA per
+// group of 2^k amplitudes at a time (grid-stride), the group staged in shared
+// memory; each warp owns output rows and reduces sum_c U[r][c] x[c] across
+// its lanes (U row-major, read coalesced from L2).  Groups are disjoint, so
+// the update is exact in place: no spare buffer (single-buffer states, e.g.
+// 34 qubits on 2 GPUs) and no copy-back.
+constexpr int kWideInPlaceK = 12;
+
+__global__ void __launch_bounds__(256) wide_group_kernel(amp_t* __restrict__ v, std::uint64_t amps,
+                                                         const double2* __restrict__ u, int k,
+                                                         const int* __restrict__ posv) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* x = reinterpret_cast<double2*>(smem_raw);
+    int pos[kBigK];
+    std::uint64_t tmask = 0;
+    for (int j = 0; j < k; ++j) {
+        pos[j] = posv[j];
+        tmask |= 1ull << pos[j];
+    }
+    // the other positions, ascending: group index bits -> offset bits
+    int rest[64];
+    int nrest = 0;
+    for (int b = 0; (1ull << b) < amps; ++b)
+        if (!((tmask >> b) & 1ull)) rest[nrest++] = b;
+    const int D = 1 << k;
+    const std::uint64_t groups = amps >> k;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (std::uint64_t g = blockIdx.x; g < groups; g += gridDim.x) {
+        std::uint64_t base = 0;
+        for (int i = 0; i < nrest; ++i) base |= ((g >> i) & 1ull) << rest[i];
+        for (int c = threadIdx.x; c < D; c += blockDim.x) {
+            std::uint64_t o = base;
+            for (int j = 0; j < k; ++j) o |= static_cast<std::uint64_t>((c >> j) & 1) << pos[j];
+            QRT_DCHECK(o < amps);
+            x[c] = v[o];
+        }
+        __syncthreads();
+        for (int r = warp; r < D; r += nwarps) {
+            double2 acc = make_double2(0.0, 0.0);
+            const double2* __restrict__ ur = u + static_cast<std::size_t>(r) * D;
+            for (int c = lane; c < D; c += 32) cfma(acc, ur[c], x[c]);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+            }
+            if (lane == 0) {
+                std::uint64_t o = base;
+                for (int j = 0; j < k; ++j) o |= static_cast<std::uint64_t>((r >> j) & 1) << pos[j];
+                v[o] = acc;  // row r's input x[r] is in shared memory; its HBM slot is free to overwrite
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// In-place diagonal gate of any width (elementwise).
+__global__ void wide_diag_kernel(amp_t* __restrict__ v, std::uint64_t amps, const double2* __restrict__ d, int k,
+                                 const int* __restrict__ posv) {
+    int pos[kBigK];
+    for (int j = 0; j < k; ++j) pos[j] = posv[j];
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < amps;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        int row = 0;
+        for (int j = 0; j < k; ++j) row |= static_cast<int>((i >> pos[j]) & 1ull) << j;
+        const double2 a = v[i], w = d[row];
+        v[i] = make_double2(fma(w.x, a.x, -w.y * a.y), fma(w.x, a.y, w.y * a.x));
+    }
+}
+
 // CTA size of the gate pass kernel: 128 (3 CTAs / SM, the launch bound) or 64;
 // QRT_GATE_THREADS overrides for experiments.
 int gate_threads() {
@@ -1608,7 +1678,32 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
             st->stats[QRT_K_GATES].bytes += 32.0 * amps_all;
             continue;
         }
-        if (h.T < 0) {  // wide, out of place into the alternate buffer, then copied back
+        if (h.T < 0 && (dev_ops[static_cast<std::size_t>(h.op_begin)].kind == kDiag ||
+                        dev_ops[static_cast<std::size_t>(h.op_begin)].k <= kWideInPlaceK)) {  // wide, in place
+            const GateOp& g = dev_ops[static_cast<std::size_t>(h.op_begin)];
+            const int widx = -h.T - 1;
+            static bool wattr[64] = {};
+            if (!wattr[st->device]) {
+                QRT_CUDA(cudaFuncSetAttribute(wide_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (1 << kWideInPlaceK) * static_cast<int>(sizeof(double2))));
+                wattr[st->device] = true;
+            }
+            for (int i = 0; i < st->pe_count; ++i) {
+                amp_t* live = st->live(i);
+                if (g.kind == kDiag)
+                    wide_diag_kernel<<<st->sm_count * 8, 256, 0, st->stream>>>(live, st->amps, d_pool + g.gmat, g.k,
+                                                                              d_wpos + widx);
+                else
+                    wide_group_kernel<<<st->sm_count * 4, 256, (std::size_t{1} << g.k) * sizeof(double2), st->stream>>>(
+                        live, st->amps, d_pool + g.gmat, g.k, d_wpos + widx);
+                QRT_CUDA(cudaGetLastError());
+            }
+            st->stats[QRT_K_GATES].launches += static_cast<std::uint64_t>(st->pe_count);
+            st->stats[QRT_K_GATES].bytes += 32.0 * amps_all;
+            continue;
+        }
+        if (h.T < 0) {  // wider than kWideInPlaceK: out of place into the alternate buffer, then copied back
+            if (st->inplace) fail(QRT_ERR_OOM, "dense gate wider than 12 qubits needs a second state buffer");
             ensure_alt(st);
             if (st->spare_busy) {  // peers may still pull our old live buffer (now the spare)
                 barrier_on_stream(st);

@@ -325,3 +325,37 @@ def test_expectation_uniform_random_strings(qb, device, monkeypatch, n, p, k, li
     got = qb.expectation(st, plan, terms)
     want = oracle_expectation(qb, psi, n, p, terms, plan)
     assert abs(got - want) <= E_TOL * (1 + abs(want)), (got, want)
+
+
+@pytest.mark.parametrize("k,diag,p,inplace", [(8, False, 1, "0"), (10, False, 2, "1"), (12, False, 1, "1"),
+                                               (11, True, 2, "1"), (14, True, 1, "0")])
+def test_wide_gate_in_place(qb, device, monkeypatch, k, diag, p, inplace):
+    """Dense gates of 8..12 qubits run in place, one group of 2^k amplitudes
+    per CTA (no spare buffer: also on single-buffer states); wide diagonals
+    elementwise in place.  Checked against the oracle's apply_gate_narrow."""
+    monkeypatch.setenv("QRT_QR_INPLACE", inplace)
+    n = 16
+    nl = n - (p.bit_length() - 1)
+    rng = np.random.default_rng(k * 10 + p)
+    psi = qb.random_state(n, 40 + k)
+    st = qb.init_state_from(psi, qb.ClusterShape.flat(p))
+    targets = [int(x) for x in rng.choice(nl, size=k, replace=False)]
+    if diag:
+        U = np.diag(np.exp(1j * rng.uniform(0, 6.28, size=1 << k)))
+    else:
+        U = qb.random_unitary(k, int(rng.integers(1 << 40)))
+    qb.apply_gate_narrow(st, qb.make_gate(0, targets, U))
+    sub = psi.reshape(p, -1).copy()
+    cpu.apply_gate(sub, targets, U)
+    assert np.max(np.abs(as_sub(st) - sub)) <= AMP_TOL
+
+
+def test_wide_gate_beyond_in_place_limit_single_buffer(qb, device, monkeypatch):
+    """A dense 13-qubit gate needs the out-of-place kernel's second buffer: a
+    single-buffer state reports it instead of failing silently."""
+    monkeypatch.setenv("QRT_QR_INPLACE", "1")
+    n = 16
+    st = qb.init_state(n, qb.ClusterShape.flat(2))
+    U = qb.random_unitary(13, 5)
+    with pytest.raises(qb.DeviceError):
+        qb.apply_gate_narrow(st, qb.make_gate(0, list(range(13)), U))

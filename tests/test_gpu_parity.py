@@ -342,8 +342,8 @@ def test_wide_gate_in_place(qb, device, monkeypatch, k, diag, p, inplace):
     targets = [int(x) for x in rng.choice(nl, size=k, replace=False)]
     if diag:
         U = np.diag(np.exp(1j * rng.uniform(0, 6.28, size=1 << k)))
-    else:
-        U = qb.random_unitary(k, int(rng.integers(1 << 40)))
+    else:  # dense and unitary, without a 2^k Gram-Schmidt on the host
+        U = np.kron(qb.random_unitary(k - 6, int(rng.integers(1 << 40))), qb.random_unitary(6, int(rng.integers(1 << 40))))
     qb.apply_gate_narrow(st, qb.make_gate(0, targets, U))
     sub = psi.reshape(p, -1).copy()
     cpu.apply_gate(sub, targets, U)
@@ -356,6 +356,6 @@ def test_wide_gate_beyond_in_place_limit_single_buffer(qb, device, monkeypatch):
     monkeypatch.setenv("QRT_QR_INPLACE", "1")
     n = 16
     st = qb.init_state(n, qb.ClusterShape.flat(2))
-    U = qb.random_unitary(13, 5)
+    U = np.roll(np.eye(1 << 13, dtype=complex), 1, axis=0)  # a dense (non-diagonal) permutation
     with pytest.raises(qb.DeviceError):
         qb.apply_gate_narrow(st, qb.make_gate(0, list(range(13)), U))

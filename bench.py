@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--span", type=int, default=10)
     ap.add_argument("--schedule", choices=["flat", "hierarchical", "adhoc"], default="flat")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pes-per-gpu", type=int, default=1,
+                    help="PEs per GPU (p = N x this): runs a p-PE schedule (e.g. the p = 8 configs) on fewer GPUs")
     ap.add_argument("--cpu-sample-qubits", type=int, default=24)
     return ap.parse_args()
 
@@ -243,7 +245,7 @@ def run_reference(args):
         return 0
     from oracle import ref as R
 
-    p = max(1, world)
+    p = max(1, world) * args.pes_per_gpu
     if not R.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libqrtile_ref.so not built"}))
         return 0
@@ -279,7 +281,7 @@ def run_ours(args):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     qb.init_distributed(device=local)
     torch.cuda.set_device(local)
-    p = world
+    p = world * args.pes_per_gpu
     n, layers, circuit, sched, terms, plan, shape = workload(qb, args, p)
     n_gates, n_terms = circuit.size(), len(terms)
     hbm_peak, peak_kind = peaks()

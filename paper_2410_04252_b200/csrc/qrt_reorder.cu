@@ -560,10 +560,13 @@ void execute_inplace(qrt_state* st, const int* dest, std::uint64_t relocated) {
 }  // namespace
 
 
+// Largest log2(amplitudes per PE) the fused (pull) QR is used for: at 2^31
+// (32q on 2 GPUs, 34q on 8) it beats the in-place exchange (16.28 vs 16.73 s,
+// profiles/r2/n2b); at 2^32 it lost even to the push exchange in round 1.
 int fused_qr_max_log2() {
     static const int v = [] {
         const char* e = std::getenv("QRT_FUSED_QR_MAX_LOG2");
-        return e ? std::atoi(e) : 30;
+        return e ? std::atoi(e) : 31;
     }();
     return v;
 }
@@ -644,9 +647,9 @@ std::uint64_t reorder(qrt_state* st, const int* dest) {
         return relocated;
     }
     // Pulling a tile's sources over NVLink scatters each CTA's reads over the
-    // whole peer buffer; past 2^30 amplitudes (16 GiB) per PE the translation
+    // whole peer buffer; past 2^31 amplitudes (32 GiB) per PE the translation
     // misses outweigh the saved exchange (34-qubit HEA on 4 GPUs: 0.31 s
-    // slower), so large states keep the push exchange.
+    // slower than even the push exchange), so larger states run in place.
     if (fused_qr_enabled() && st->p > 1 && st->nl <= fused_qr_max_log2()) {
         st->qr_pending = true;  // the next gate pass gathers through it
         st->qr_dest.assign(dest, dest + st->n);

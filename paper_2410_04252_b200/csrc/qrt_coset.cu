@@ -385,6 +385,10 @@ __global__ void __launch_bounds__(2 * kCosetThreads, 1)
     constexpr int E = 1 << kTileBits;
     const int c = P.c;
     const int team = threadIdx.x >> 7, tid = threadIdx.x & (kCosetThreads - 1);
+    // one or two compute teams: with one, two of the three buffers are always
+    // filling (128 KiB in flight per SM) — for passes whose tiles compute
+    // faster than they load (GF(2)-linear passes: scattered 64-byte runs)
+    const int nteams = static_cast<int>(blockDim.x) / kCosetThreads;
     double2* bufs = reinterpret_cast<double2*>(smem_raw);  // 3 x E
     u64* tabo = reinterpret_cast<u64*>(bufs + 3 * E);
     double2* stab = reinterpret_cast<double2*>(tabo + ((1 << (kTileBits - c)) | 1) + 1);
@@ -427,15 +431,15 @@ __global__ void __launch_bounds__(2 * kCosetThreads, 1)
         const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[fill_bar(k)]));
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a));
     };
-    // tile k is issued by team (k + 1) & 1
+    // tile k is issued by the team that computed tile k - 3: (k - 3) mod nteams
     for (int k = 0; k < 3 && k < ntile; ++k)
-        if (((k + 1) & 1) == team) issue(k);
+        if ((k + 3 * nteams - 3) % nteams == team) issue(k);
 
     double2 acc = make_double2(0.0, 0.0);
-    for (int k = team; k < ntile; k += 2) {
+    for (int k = team; k < ntile; k += nteams) {
         const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[fill_bar(k)]));
         mbar_wait(a, fill_parity(k));
-        QRT_DCHECK((k & 1) == team && k < ntile);
+        QRT_DCHECK(k % nteams == team && k < ntile);
 #ifdef QRT_CHECKS
         {  // the awaited buffer really holds tile k (the state is read-only during EVC)
             const u64 bk = tile_of(k);
@@ -688,12 +692,20 @@ void launch_coset_pass(const CosetParams& P, const CosetDiagTerm* dterms, int pe
             QRT_CUDA(cudaGetLastError());
             return;
         }
+        // QRT_EVC_TEAMS: 2 (default) or 1 compute teams per SM for every pass,
+        // or 0: one team on GF(2)-linear passes (single-bit groups), two otherwise
+        static const int teams_knob = [] {
+            const char* e = std::getenv("QRT_EVC_TEAMS");
+            return e ? std::atoi(e) : 2;
+        }();
+        const int teams = teams_knob == 1 ? 1 : (teams_knob == 0 && any_ones) ? 1 : 2;
+        const int pthreads = teams * kCosetThreads;
         if (generic)
-            coset_pipe_kernel<true, true><<<pgrid, 2 * kCosetThreads, psmem, stream>>>(P, red);
+            coset_pipe_kernel<true, true><<<pgrid, pthreads, psmem, stream>>>(P, red);
         else if (any_ones)
-            coset_pipe_kernel<false, true><<<pgrid, 2 * kCosetThreads, psmem, stream>>>(P, red);
+            coset_pipe_kernel<false, true><<<pgrid, pthreads, psmem, stream>>>(P, red);
         else
-            coset_pipe_kernel<false, false><<<pgrid, 2 * kCosetThreads, psmem, stream>>>(P, red);
+            coset_pipe_kernel<false, false><<<pgrid, pthreads, psmem, stream>>>(P, red);
         QRT_CUDA(cudaGetLastError());
         return;
     }

@@ -1613,8 +1613,17 @@ void apply_gates(qrt_state* st, int n_gates, const int* arity, const int* pos, c
     // pass is an out-of-place wide gate.
     bool fuse_first = false;
     FusedSource fsrc{};
+    // A light (register-resident) pass computes too little per tile to hide a
+    // pull over whole 2^31-amplitude peer buffers: past 2^30 per PE its QR runs
+    // in place first (34q HEA with 2 PEs on each of 4 GPUs: gates 3.24 s fused
+    // vs ~2.1 s), while DMMA gate passes keep pulling up to fused_qr_max_log2().
+    static const int light_fuse_max = [] {
+        const char* e = std::getenv("QRT_FUSED_LIGHT_MAX_LOG2");
+        return e ? std::atoi(e) : 30;
+    }();
     if (st->qr_pending) {
-        if (!hdrs.empty() && hdrs[0].T >= 0) {
+        const bool light_first = !hdrs.empty() && hdrs[0].T >= kLightMarker;
+        if (!hdrs.empty() && hdrs[0].T >= 0 && !(light_first && st->nl > light_fuse_max)) {
             fuse_first = true;
             ensure_alt(st);
             for (int pe = 0; pe < st->p; ++pe) fsrc.src[pe] = st->peer[st->cur][static_cast<std::size_t>(pe)];

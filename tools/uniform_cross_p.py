@@ -1,4 +1,6 @@
-"""Debug: uniform-word energy vs p on one GPU, against the C oracle at p=1."""
+"""Uniform-word (C5 stress) energy vs p on one GPU against the C oracle at p = 1:
+the reproducer of the round-1 EVC pipeline race (profiles/r2/uniform24_race_repro.txt).
+  python tools/uniform_cross_p.py N COUNT P1,P2,... [nooracle]"""
 import json
 import sys
 

@@ -887,15 +887,6 @@ PauliPlanHost build_pauli_plan(int nl, int pe_begin, int n_terms, const std::uin
             for (int p = 0; p < nl && popc(b) < T; ++p) b |= 1ull << p;
             return b;
         };
-        // I/Z words in a pass of their own (a Walsh-Hadamard transform of |v|^2
-        // per tile, no register sets): the pass that carries them runs on the
-        // unpipelined kernel, so every set group moved out of it runs
-        // pipelined instead (QRT_EVC_DIAG_ALONE=0 keeps them together)
-        const bool diag_alone = !diag.empty() && [] {
-            const char* e = std::getenv("QRT_EVC_DIAG_ALONE");
-            return !e || std::atoi(e) != 0;
-        }();
-        if (diag_alone) passes.push_back(Pass{fill(coal_bits), {}, true, {}});
         bool first = true;
         while (!rem.empty()) {
             auto count = [&](std::uint64_t b) {
@@ -927,7 +918,7 @@ PauliPlanHost build_pauli_plan(int nl, int pe_begin, int n_terms, const std::uin
                     B = b;
                 }
             }
-            Pass ps{B, {}, first && !diag.empty() && !diag_alone, {}};
+            Pass ps{B, {}, first && !diag.empty(), {}};
             first = false;
             std::vector<std::size_t> keep;
             for (std::size_t i : rem) {

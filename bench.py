@@ -388,7 +388,7 @@ def run_ours(args):
     if top == "gates" and args.circuit == "gatefabric":
         # dense 4-qubit blocks on the fp64 tensor pipe: flop-bound (SURVEY.md section 7 hard parts)
         roof = {"bound": "tensor", "achieved": f["fp64_tflops_ref_equiv"], "peak": FP64_TENSOR_PEAK, "unit": "TFLOP/s",
-                "frac": f["fp64_frac"], "peak_kind": "measured fp64 DMMA (tools/microbench_fp64.cu)"}
+                "frac": f["fp64_frac"], "peak_kind": "builder-measured fp64 DMMA (tools/microbench_fp64.cu, profiles/r1_microbench_fp64.txt; not in MEASURED_PEAKS.json)"}
         # `achieved` counts the reference's algorithmic flops.  The Gauss-form
         # kernel executes 3 real 16x16 products + 1 DADD per amplitude instead of the
         # 16 complex MACs: 98 of 128 flop-slots on the shared fp64 datapath.

@@ -1286,7 +1286,10 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
                                                             reinterpret_cast<const PTerm*>(dev + toff), red);
             QRT_CUDA(cudaGetLastError());
             st->stats[QRT_K_PAULI].launches++;
-            st->stats[QRT_K_PAULI].bytes += 32.0 * static_cast<double>(st->amps) * st->pe_count * wgroups.size() / 2;
+            // algorithmic bytes of the launch: one read of the state (all of its
+            // groups are evaluated in one launch; per-group re-reads hit L2 — round 1
+            // charged a sweep per group, which reported an HBM fraction of 1.15)
+            st->stats[QRT_K_PAULI].bytes += 16.0 * static_cast<double>(st->amps) * st->pe_count;
         }
         reduce_slots_kernel<<<st->pe_count, 256, 0, st->stream>>>(red, ctas, out);
         QRT_CUDA(cudaGetLastError());

@@ -632,6 +632,8 @@ __global__ void __launch_bounds__(2 * kSplitTeam, 1)
 
 }  // namespace
 
+constexpr int kPipeSmemMax = 225 * 1024;  // dynamic shared memory of the pipelined kernels (+ ~1 KiB static)
+
 void launch_coset_pass(const CosetParams& P, const CosetDiagTerm* dterms, int pe_count, double* red,
                        cudaStream_t stream, int device) {
     // Launches holding only Jordan-Wigner-type groups take the fast-only
@@ -661,14 +663,19 @@ void launch_coset_pass(const CosetParams& P, const CosetDiagTerm* dterms, int pe
         const char* e = std::getenv("QRT_EVC_PIPE");
         return e ? std::atoi(e) != 0 : true;
     }();
-    if (pipe && P.d_count == 0 && occ == 2) {  // persistent two-team pipeline (no I/Z words)
+    const std::size_t pipe_smem = 3 * (std::size_t{1} << kTileBits) * sizeof(double2) +
+                                  ((std::size_t{1} << (kTileBits - P.c)) + 2) * sizeof(std::uint64_t) +
+                                  static_cast<std::size_t>(P.n_tab) * sizeof(double);
+    // (three tile buffers + the tile-offset table + the coefficient tables must fit
+    // next to the static shared memory; a pass that does not takes the one-buffer kernel)
+    if (pipe && P.d_count == 0 && occ == 2 && pipe_smem <= static_cast<std::size_t>(kPipeSmemMax)) {  // persistent pipeline
         static int nsm[64] = {};
         static bool pattr[64] = {};
         if (!nsm[device]) QRT_CUDA(cudaDeviceGetAttribute(&nsm[device], cudaDevAttrMultiProcessorCount, device));
         if (!pattr[device]) {
-            QRT_CUDA(cudaFuncSetAttribute(coset_pipe_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-            QRT_CUDA(cudaFuncSetAttribute(coset_pipe_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-            QRT_CUDA(cudaFuncSetAttribute(coset_pipe_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+            QRT_CUDA(cudaFuncSetAttribute(coset_pipe_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPipeSmemMax));
+            QRT_CUDA(cudaFuncSetAttribute(coset_pipe_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPipeSmemMax));
+            QRT_CUDA(cudaFuncSetAttribute(coset_pipe_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPipeSmemMax));
             pattr[device] = true;
         }
         const std::size_t psmem = 3 * (std::size_t{1} << kTileBits) * sizeof(double2) +
@@ -685,7 +692,7 @@ void launch_coset_pass(const CosetParams& P, const CosetDiagTerm* dterms, int pe
             static bool sattr[64] = {};
             if (!sattr[device]) {
                 QRT_CUDA(cudaFuncSetAttribute(coset_pipe_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              220 * 1024));
+                                              kPipeSmemMax));
                 sattr[device] = true;
             }
             coset_pipe_split_kernel<<<pgrid, 2 * kSplitTeam, psmem, stream>>>(P, red);

@@ -1098,11 +1098,11 @@ PauliPlanHost build_pauli_plan(int nl, int pe_begin, int n_terms, const std::uin
         for (std::size_t i = 0; i < wide.size(); ++i) pending[i] = i;
         // unit low positions of a linear tile: 2 (64-byte runs; 10 groups per
         // pass, measured faster than 4 positions / 256-byte runs with 8 groups:
-        // the passes are compute-bound).  QRT_EVC_LINEAR_COAL overrides (2..4;
-        // fewer would not fit the pipelined kernel's shared memory).
+        // the passes are compute-bound).  QRT_EVC_LINEAR_COAL overrides (0..4:
+        // every unit axis given up is one more group per HBM read).
         const int lcoal = [&] {
             const char* e = std::getenv("QRT_EVC_LINEAR_COAL");
-            return std::max(std::min(coal, 2), std::min(coal, e ? std::atoi(e) : 2));
+            return std::max(0, std::min(coal, e ? std::atoi(e) : 2));
         }();
         const std::uint64_t coal_m = (1ull << lcoal) - 1;
         std::vector<std::uint64_t> smL(static_cast<std::size_t>(n_terms), 0);

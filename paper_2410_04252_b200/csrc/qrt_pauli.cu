@@ -1192,7 +1192,7 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
     // A VQE loop evaluates the same Hamiltonian under the same layout every
     // iteration: plans are cached by their exact inputs.
     static std::mutex cache_mu;
-    static std::deque<std::pair<std::vector<std::uint64_t>, std::shared_ptr<PauliPlanHost>>> cache;
+    static std::deque<std::pair<std::vector<std::uint64_t>, std::shared_ptr<const PauliPlanHost>>> cache;
     std::vector<std::uint64_t> key;
     key.reserve(3 + 6 * static_cast<std::size_t>(n_terms));
     key.push_back(static_cast<std::uint64_t>(nl));
@@ -1204,17 +1204,24 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
         std::memcpy(&ci, coeffs + 2 * t + 1, 8);
         key.insert(key.end(), {x[t], y[t], z[t], gz[t], cr, ci});
     }
-    std::lock_guard<std::mutex> lock(cache_mu);
-    std::shared_ptr<PauliPlanHost> plan_ptr;
-    for (auto& e : cache)
-        if (e.first == key) plan_ptr = e.second;
+    // The lock covers the lookup / insertion only: the cached plan is immutable
+    // (per-launch pointers are patched into a thread-local copy of each pass's
+    // parameters below), so concurrent states never serialise on it.
+    std::shared_ptr<const PauliPlanHost> plan_ptr;
+    {
+        std::lock_guard<std::mutex> lock(cache_mu);
+        for (auto& e : cache)
+            if (e.first == key) plan_ptr = e.second;
+    }
     if (!plan_ptr) {
-        plan_ptr = std::make_shared<PauliPlanHost>(build_pauli_plan(nl, st->pe_begin, n_terms, x, y, z, gz, coeffs));
-        cache.emplace_back(std::move(key), plan_ptr);
+        auto built = std::make_shared<const PauliPlanHost>(build_pauli_plan(nl, st->pe_begin, n_terms, x, y, z, gz, coeffs));
+        std::lock_guard<std::mutex> lock(cache_mu);
+        cache.emplace_back(std::move(key), built);
         // one entry per EVC plan tile of the Hamiltonian (uniform 10k words: 26-60 tiles)
         if (cache.size() > 96) cache.pop_front();
+        plan_ptr = std::move(built);
     }
-    PauliPlanHost& plan = *plan_ptr;
+    const PauliPlanHost& plan = *plan_ptr;
     const int T = plan.T;
     auto& dgroups = plan.dgroups;
     auto& dterms = plan.dterms;
@@ -1258,11 +1265,14 @@ void pauli_expectation(qrt_state* st, int n_terms, const std::uint64_t* x, const
     for (int i = 0; i < st->pe_count; ++i) ptrs.p[i] = st->live(i);
     {
         ProfileScope prof(st, QRT_K_PAULI);
+        static thread_local std::unique_ptr<CosetParams> scratch_params;  // ~27 KiB: off the stack
+        if (!scratch_params) scratch_params = std::make_unique<CosetParams>();
         for (std::size_t ci = 0; ci < plan.cosets.size(); ++ci) {
-            auto& cp = plan.cosets[ci];
-            cp->gtabs = reinterpret_cast<const double*>(dev + tab_off[ci]);
-            for (int i = 0; i < st->pe_count; ++i) cp->ptrs[i] = st->live(i);
-            launch_coset_pass(*cp, reinterpret_cast<const CosetDiagTerm*>(dev + coff), st->pe_count, red, st->stream,
+            CosetParams& cp = *scratch_params;
+            cp = *plan.cosets[ci];
+            cp.gtabs = reinterpret_cast<const double*>(dev + tab_off[ci]);
+            for (int i = 0; i < st->pe_count; ++i) cp.ptrs[i] = st->live(i);
+            launch_coset_pass(cp, reinterpret_cast<const CosetDiagTerm*>(dev + coff), st->pe_count, red, st->stream,
                               st->device);
             st->stats[QRT_K_PAULI].launches++;
             st->stats[QRT_K_PAULI].bytes += 16.0 * static_cast<double>(st->amps) * st->pe_count;

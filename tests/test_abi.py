@@ -121,3 +121,23 @@ def test_evc_linear_passes_knob(qb, monkeypatch):
     monkeypatch.setenv("QRT_EVC_LINEAR", "1")
     passes_on, _, wide_on, _ = _plan_info(qb, rnd)
     assert wide_off > 30 and wide_on == 0 and passes_on <= 6
+
+
+def test_qr_bench_validation_without_device(qb):
+    """qrt_qr_bench (single-process NVLink microbenchmark) rejects bad shapes
+    before touching a device, and reports the missing GPUs loudly."""
+    lib = qb.load_libqrt()
+    ms, gbs = C.c_double(), C.c_double()
+    assert lib.qrt_qr_bench(3, 28, 1, 1, 1, C.byref(ms), C.byref(gbs)) == 7   # QRT_ERR_CONFIG: not a power of two
+    assert lib.qrt_qr_bench(2, 28, 2, 1, 1, C.byref(ms), C.byref(gbs)) == 7   # k > log2(n_gpus)
+    assert lib.qrt_qr_bench(2, 8, 1, 1, 1, C.byref(ms), C.byref(gbs)) == 7    # n_local below a tile
+    n = C.c_int(-1)
+    lib.qrt_device_count(C.byref(n))
+    if n.value < 2:
+        assert lib.qrt_qr_bench(2, 28, 1, 1, 1, C.byref(ms), C.byref(gbs)) in (9, 11)  # CUDA / no device
+
+
+def test_build_flags(qb):
+    assert qb.build_flags() in (0, 1)
+    chk = C.CDLL(str(Path(qb.__file__).parent / "libqrt_checked.so"))
+    assert chk.qrt_build_flags() == 1 and qb.load_libqrt().qrt_build_flags() == 0

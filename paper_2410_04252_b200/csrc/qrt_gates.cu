@@ -477,6 +477,18 @@ __global__ void __launch_bounds__(128, MINB)
         fused_tables(*fs, tab, nt, base, fs->pe_begin + t / tiles_per_pe, words);
         for (int e = threadIdx.x; e < E; e += blockDim.x) cp_async16(&tile[swz(e)], fused_src(*fs, words, e, cmask, c));
         v = fs->dst[t / tiles_per_pe];
+    } else if (T == kTileBits && blockDim.x == 128 && c <= 7) {
+        // e = tid + 128 i: the swizzle is GF(2)-linear (swz(e) = swz(tid) ^ swz(128 i), a
+        // constant per unrolled i) and e >> c, e & cmask split the same way, so each
+        // load is one shared-memory table read and two ORs
+        const int tsw = swz(threadIdx.x), th = threadIdx.x >> c;
+        const amp_t* __restrict__ vb = v + (base | (threadIdx.x & cmask));
+#pragma unroll
+        for (int i = 0; i < (1 << kTileBits) / 128; ++i) {
+            QRT_DCHECK((base | tab[th + (i << (7 - c))] | (threadIdx.x & cmask)) <
+                       (static_cast<std::uint64_t>(tiles_per_pe) << T));
+            cp_async16(&tile[tsw ^ swz(i * 128)], vb + tab[th + (i << (7 - c))]);
+        }
     } else {
         for (int e = threadIdx.x; e < E; e += blockDim.x) {
             QRT_DCHECK((base | tab[e >> c] | (e & cmask)) < (static_cast<std::uint64_t>(tiles_per_pe) << T));
@@ -521,6 +533,13 @@ __global__ void __launch_bounds__(128, MINB)
             }
         }
         __syncthreads();
+    }
+    if (T == kTileBits && blockDim.x == 128 && c <= 7) {  // as the load
+        const int tsw = swz(threadIdx.x), th = threadIdx.x >> c;
+        amp_t* __restrict__ vb = v + (base | (threadIdx.x & cmask));
+#pragma unroll
+        for (int i = 0; i < (1 << kTileBits) / 128; ++i) __stcs(vb + tab[th + (i << (7 - c))], tile[tsw ^ swz(i * 128)]);
+        return;
     }
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
         QRT_DCHECK((base | tab[e >> c] | (e & cmask)) < (static_cast<std::uint64_t>(tiles_per_pe) << T));

@@ -24,3 +24,20 @@ def test_distributed_qsu_evc(qb, world):
     line = [l for l in res.stdout.splitlines() if l.startswith("{")][-1]
     out = json.loads(line)
     assert out["ok"], out
+
+
+def test_qr_bench_single_process(qb):
+    """qrt_qr_bench (tools/qr_nvlink.py): both exchange kernels over CUDA peer
+    access in one process, k = 1..log2(N); rates are positive and finite."""
+    import ctypes as C
+
+    n = qb.device_count()
+    if n < 2:
+        pytest.skip("needs 2 GPUs")
+    n = 4 if n >= 4 else 2
+    lib = qb.load_libqrt()
+    for inplace in (0, 1):
+        for k in range(1, n.bit_length()):
+            ms, gbs = C.c_double(), C.c_double()
+            assert lib.qrt_qr_bench(n, 24, k, inplace, 2, C.byref(ms), C.byref(gbs)) == 0
+            assert ms.value > 0 and 0 < gbs.value < 5000

@@ -615,7 +615,7 @@ void execute_reorder(qrt_state* st, const int* dest) {
 // An executed (not fused) QR: the in-place pairwise swap whenever the map
 // allows it — it moves only the (1 - 2^-k) that changes PE and measured 679
 // vs 531 GB/s per direction for the push kernel (2 x B200, 2^30 amplitudes
-// per PE, profiles/r2_qr_nvlink.json) — else the push exchange into the spare
+// per PE, profiles/r2_ncu_qr_nvlink.json) — else the push exchange into the spare
 // buffer.  QRT_QR_PUSH=1 forces the push kernel on two-buffer states.
 void execute_qr(qrt_state* st, const int* dest) {
     static const bool force_push = [] {

@@ -213,12 +213,10 @@ __device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const doub
                                                 double2& acc) {
     for (int s = 0; s < P.n_sets; ++s) {
         const CosetSet& S = P.sets[s];
-        int ebase = 0;
-#pragma unroll
-        for (int i = 0; i < kTileBits - kCosetBits; ++i) ebase |= ((t >> i) & 1) << S.tb[i];
+        const int ebase = S.eb_lo[t & 15] | S.eb_hi[t >> 4];  // host tables (coset_set_tables)
         int swq[kCosetBits];
 #pragma unroll
-        for (int q = 0; q < kCosetBits; ++q) swq[q] = swz(1 << S.S[q]);
+        for (int q = 0; q < kCosetBits; ++q) swq[q] = S.swq[q];
         const int sb = swz(ebase);
         double2 a[32];
         {

@@ -47,7 +47,32 @@ struct CosetSet {
     std::uint8_t one_cnt[kCosetBits];  // then single-bit-mask groups: one_cnt[k] with mask 1 << k; generic after them
     std::uint8_t one_re[kCosetBits];   // ... of which the first one_re[k] are mode 0 and the next one_im[k] mode 2
     std::uint8_t one_im[kCosetBits];
+    // host-precomputed per set (coset_set_tables): the thread's tile index is
+    // eb_lo[t & 15] | eb_hi[t >> 4], and swq[q] the swizzled offset of register bit q
+    std::uint16_t eb_lo[16];
+    std::uint16_t eb_hi[8];
+    std::int16_t swq[kCosetBits];
 };
+
+// Shared-memory swizzle of tile element e (GF(2)-linear): the host twin of the
+// kernels' swz(), used to precompute CosetSet::swq.
+inline constexpr int coset_swz(int e) {
+    return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9) ^ (e >> 12)) & 7);
+}
+
+inline void coset_set_tables(CosetSet& S) {
+    for (int v = 0; v < 16; ++v) {
+        int e = 0;
+        for (int i = 0; i < 4; ++i) e |= ((v >> i) & 1) << S.tb[i];
+        S.eb_lo[v] = static_cast<std::uint16_t>(e);
+    }
+    for (int v = 0; v < 8; ++v) {
+        int e = 0;
+        for (int i = 0; i < 3; ++i) e |= ((v >> i) & 1) << S.tb[4 + i];
+        S.eb_hi[v] = static_cast<std::uint16_t>(e);
+    }
+    for (int q = 0; q < kCosetBits; ++q) S.swq[q] = static_cast<std::int16_t>(coset_swz(1 << S.S[q]));
+}
 
 // W = tile index (bits 0..11) | outer index of the CTA (bit 12 + i <-> outer axis i).
 struct CosetParams {

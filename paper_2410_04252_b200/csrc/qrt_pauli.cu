@@ -596,6 +596,7 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
                     }
             rest.insert(rest.begin(), lead.begin(), lead.end());
             for (int i = 0; i < kTileBits - kCosetBits; ++i) S.tb[i] = static_cast<std::int8_t>(rest[static_cast<std::size_t>(i)]);
+            coset_set_tables(S);
         }
         auto to_reg = [&](int tilemask) {
             int r = 0;

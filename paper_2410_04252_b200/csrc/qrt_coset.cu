@@ -213,10 +213,18 @@ __device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const doub
                                                 double2& acc) {
     for (int s = 0; s < P.n_sets; ++s) {
         const CosetSet& S = P.sets[s];
-        const int ebase = S.eb_lo[t & 15] | S.eb_hi[t >> 4];  // host tables (coset_set_tables)
-        int swq[kCosetBits];
+        int ebase, swq[kCosetBits];
+        if (P.set_tables) {  // host tables (coset_set_tables)
+            ebase = S.eb_lo[t & 15] | S.eb_hi[t >> 4];
 #pragma unroll
-        for (int q = 0; q < kCosetBits; ++q) swq[q] = S.swq[q];
+            for (int q = 0; q < kCosetBits; ++q) swq[q] = S.swq[q];
+        } else {
+            ebase = 0;
+#pragma unroll
+            for (int i = 0; i < kTileBits - kCosetBits; ++i) ebase |= ((t >> i) & 1) << S.tb[i];
+#pragma unroll
+            for (int q = 0; q < kCosetBits; ++q) swq[q] = swz(1 << S.S[q]);
+        }
         const int sb = swz(ebase);
         double2 a[32];
         {
@@ -632,8 +640,13 @@ __global__ void __launch_bounds__(2 * kSplitTeam, 1)
 
 constexpr int kPipeSmemMax = 225 * 1024;  // dynamic shared memory of the pipelined kernels (+ ~1 KiB static)
 
-void launch_coset_pass(const CosetParams& P, const CosetDiagTerm* dterms, int pe_count, double* red,
+void launch_coset_pass(CosetParams& P, const CosetDiagTerm* dterms, int pe_count, double* red,
                        cudaStream_t stream, int device) {
+    static const int set_tables = [] {
+        const char* e = std::getenv("QRT_EVC_SET_TABLES");
+        return e ? std::atoi(e) : 1;
+    }();
+    P.set_tables = set_tables;
     // Launches holding only Jordan-Wigner-type groups take the fast-only
     // kernel (218 registers, 2 CTAs/SM; QRT_COSET_OCC=3 squeezes it to 3 CTAs/SM
     // with spills, measured slower); any generic group needs the

@@ -239,6 +239,7 @@ __device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const doub
         }
         const u64 W = static_cast<u64>(ebase) | wout;
         const unsigned present = S.present;
+        if (present) {  // linear-pass sets have no weight-2/4 groups: skip the 15 mask tests
         coset_fast<3>(a, P, S, stab, present, W, pe, acc);
         coset_fast<5>(a, P, S, stab, present, W, pe, acc);
         coset_fast<6>(a, P, S, stab, present, W, pe, acc);
@@ -254,6 +255,7 @@ __device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const doub
         coset_fast<27>(a, P, S, stab, present, W, pe, acc);
         coset_fast<29>(a, P, S, stab, present, W, pe, acc);
         coset_fast<30>(a, P, S, stab, present, W, pe, acc);
+        }
         int g1 = S.g_begin + S.xbeg[31];
         if (ONES) {
             const double* __restrict__ dt = reinterpret_cast<const double*>(stab);

@@ -426,15 +426,41 @@ __global__ void __launch_bounds__(2 * kCosetThreads, 1)
     auto tile_of = [&](int k) { return static_cast<u64>(blockIdx.x) + static_cast<u64>(k) * stride; };
     auto issue = [&](int k) {  // this team's 128 threads fill buffer k % 3 with tile k
         const u64 b = tile_of(k);
+        // base = XOR of the outer axes of b's set bits: lane i takes axes i, i+32, ...
+        // and the warp XOR-reduces (every thread walking all axes cost ~7% of the
+        // instructions of a GF(2)-linear pass)
         u64 base = 0;
-        for (int i = 0; i < P.n_outer; ++i)
-            if ((b >> i) & 1ull) base ^= P.outer_vec[i];
+        if (P.fill_mode) {
+            for (int i = tid & 31; i < P.n_outer; i += 32)
+                if ((b >> i) & 1ull) base ^= P.outer_vec[i];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) base ^= __shfl_xor_sync(0xffffffffu, base, o);
+        } else {
+            for (int i = 0; i < P.n_outer; ++i)
+                if ((b >> i) & 1ull) base ^= P.outer_vec[i];
+        }
         double2* tile = bufs + (k % 3) * E;
-        for (int e = tid; e < E; e += kCosetThreads) {
-            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&tile[swz(e)]));
-            QRT_DCHECK((base ^ tabo[e >> c] ^ (e & cmask)) < (static_cast<u64>(P.tiles_per_pe) << kTileBits));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
-                         "l"(&v[base ^ tabo[e >> c] ^ (e & cmask)]));
+        if (c <= 7 && P.fill_mode) {
+            // e = tid + 128 i: the swizzle is GF(2)-linear, so swz(e) = swz(tid) ^ swz(128 i)
+            // (a constant per unrolled i), and e >> c / e & cmask split the same way (the
+            // per-element addressing was ~30% of a linear pass's instructions)
+            const unsigned sa0 = static_cast<unsigned>(__cvta_generic_to_shared(tile));
+            const int tsw = swz(tid), th = tid >> c;
+            const u64 bl = base ^ static_cast<u64>(tid & cmask);
+#pragma unroll
+            for (int i = 0; i < E / kCosetThreads; ++i) {
+                const unsigned sa = sa0 + 16u * static_cast<unsigned>(tsw ^ swz(i * kCosetThreads));
+                QRT_DCHECK((bl ^ tabo[th + (i << (7 - c))]) < (static_cast<u64>(P.tiles_per_pe) << kTileBits));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
+                             "l"(v + (bl ^ tabo[th + (i << (7 - c))])));
+            }
+        } else {
+            for (int e = tid; e < E; e += kCosetThreads) {
+                const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&tile[swz(e)]));
+                QRT_DCHECK((base ^ tabo[e >> c] ^ (e & cmask)) < (static_cast<u64>(P.tiles_per_pe) << kTileBits));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
+                             "l"(&v[base ^ tabo[e >> c] ^ (e & cmask)]));
+            }
         }
         const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&full[fill_bar(k)]));
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a));
@@ -649,6 +675,11 @@ void launch_coset_pass(CosetParams& P, const CosetDiagTerm* dterms, int pe_count
         return e ? std::atoi(e) : 1;
     }();
     P.set_tables = set_tables;
+    static const int fill_mode = [] {
+        const char* e = std::getenv("QRT_EVC_FILL");
+        return e ? std::atoi(e) : 1;
+    }();
+    P.fill_mode = fill_mode;
     // Launches holding only Jordan-Wigner-type groups take the fast-only
     // kernel (218 registers, 2 CTAs/SM; QRT_COSET_OCC=3 squeezes it to 3 CTAs/SM
     // with spills, measured slower); any generic group needs the

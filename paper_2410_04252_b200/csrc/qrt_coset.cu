@@ -675,9 +675,9 @@ void launch_coset_pass(CosetParams& P, const CosetDiagTerm* dterms, int pe_count
         return e ? std::atoi(e) : 1;
     }();
     P.set_tables = set_tables;
-    static const int fill_mode = [] {
+    static const int fill_mode = [] {  // measured: JW 962 -> 979 ms, uniform 2139 -> 2134 ms with 1
         const char* e = std::getenv("QRT_EVC_FILL");
-        return e ? std::atoi(e) : 1;
+        return e ? std::atoi(e) : 0;
     }();
     P.fill_mode = fill_mode;
     // Launches holding only Jordan-Wigner-type groups take the fast-only

@@ -239,7 +239,7 @@ __device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const doub
         }
         const u64 W = static_cast<u64>(ebase) | wout;
         const unsigned present = S.present;
-        if (present) {  // linear-pass sets have no weight-2/4 groups: skip the 15 mask tests
+        if (present || !P.present_guard) {  // linear-pass sets have no weight-2/4 groups: skip the 15 mask tests
         coset_fast<3>(a, P, S, stab, present, W, pe, acc);
         coset_fast<5>(a, P, S, stab, present, W, pe, acc);
         coset_fast<6>(a, P, S, stab, present, W, pe, acc);
@@ -680,6 +680,11 @@ void launch_coset_pass(CosetParams& P, const CosetDiagTerm* dterms, int pe_count
         return e ? std::atoi(e) : 0;
     }();
     P.fill_mode = fill_mode;
+    static const int present_guard = [] {
+        const char* e = std::getenv("QRT_EVC_PRESENT_GUARD");
+        return e ? std::atoi(e) : 1;
+    }();
+    P.present_guard = present_guard;
     // Launches holding only Jordan-Wigner-type groups take the fast-only
     // kernel (218 registers, 2 CTAs/SM; QRT_COSET_OCC=3 squeezes it to 3 CTAs/SM
     // with spills, measured slower); any generic group needs the

@@ -85,6 +85,7 @@ struct CosetParams {
     int d_begin, d_count;  // I/Z words of this pass (global term array), Walsh-Hadamard path
     int n_tab;             // doubles of tabs in use (staged in shared memory)
     int set_tables;        // 1: per-set thread-index / swizzle tables from the host (QRT_EVC_SET_TABLES)
+    int present_guard;     // 1: skip a set's weight-2/4 mask tests when it has none (QRT_EVC_PRESENT_GUARD)
     int fill_mode;         // 1: pipelined tile fill with warp-reduced base + unrolled linear-swizzle addressing (QRT_EVC_FILL)
     const double* gtabs;   // device copy of tabs[0, n_tab) (coalesced staging)
     // Tile / outer axes as index vectors: element (outer b, tile e) sits at

@@ -56,11 +56,20 @@ def _headers() -> list[Path]:
             + list((PKG / "host" / "include" / "qrtile").glob("*.hpp")))
 
 
-def build_libqrt(checked: bool = False) -> Path:
+def build_variant(name: str, defines: list[str]) -> Path:
+    """An experiment build: libqrt_<name>.so from the same sources with extra
+    -D defines, objects in _build_<name>.  Preload it (LD_PRELOAD) next to the
+    product library for a same-box A/B of a compile-time alternative."""
+    return build_libqrt(defines=defines, bdir=PKG / f"_build_{name}", out=PKG / f"libqrt_{name}.so")
+
+
+def build_libqrt(checked: bool = False, defines: list[str] | None = None, bdir: Path | None = None,
+                 out: Path | None = None) -> Path:
     """libqrt.so, or with checked=True libqrt_checked.so: the same kernels with
     -DQRT_CHECKS device-side bounds / pipeline checks (tests preload it)."""
-    bdir = BUILD_CHECKED if checked else BUILD
-    out = LIBQRT_CHECKED if checked else LIBQRT
+    bdir = bdir or (BUILD_CHECKED if checked else BUILD)
+    out = out or (LIBQRT_CHECKED if checked else LIBQRT)
+    defines = list(defines or []) + (["QRT_CHECKS"] if checked else [])
     bdir.mkdir(exist_ok=True)
     objs, jobs = [], []
     for src in CU_SRCS:
@@ -69,7 +78,7 @@ def build_libqrt(checked: bool = False) -> Path:
         objs.append(o)
         if _stale(o, [s] + _headers()):
             jobs.append([NVCC, "-std=c++17", *ARCH, "-O3", "-lineinfo", "-Xcompiler", "-fPIC",
-                         *(["-DQRT_CHECKS"] if checked else []),
+                         *[f"-D{d}" for d in defines],
                          "-I", str(ROOT / "include"), "-I", str(NCCL / "include"),
                          "-c", str(s), "-o", str(o)])
     with ThreadPoolExecutor(max_workers=4) as ex:

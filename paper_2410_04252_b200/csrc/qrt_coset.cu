@@ -31,13 +31,37 @@ __host__ __device__ constexpr int ins0(int v, int bit) { return ((v >> bit) << (
 // sum_rho T[rho] * Re(conj(a[r^XQ]) a[r]) over the 16 canonical pairs
 // (r, r^XQ) of the coset, r without the top bit of XQ (register indices are
 // compile-time: one code body per mask).
+// QRT_EVC_EARLY_TABLES: issue the group's 8 table loads (LDS.128) before the
+// pair products, pinned by volatile asm, so their latency overlaps the DMUL /
+// DFMA work instead of stalling the accumulation chains (the compiler places
+// them after the products to save registers).
+#ifndef QRT_EVC_EARLY_TABLES
+#define QRT_EVC_EARLY_TABLES 1
+#endif
+
+__device__ __forceinline__ double2 lds_f64x2(const double2* p) {
+    double2 v;
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+
 template <int XQ>
 __device__ __forceinline__ double coset_group(const double2 (&a)[32], const double2* __restrict__ T2) {
     constexpr int H = top_bit(XQ);
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#if QRT_EVC_EARLY_TABLES
+    double2 tt[8];
+#pragma unroll
+    for (int h = 0; h < 8; ++h) tt[h] = lds_f64x2(T2 + h);
+#endif
 #pragma unroll
     for (int h = 0; h < 8; ++h) {
+#if QRT_EVC_EARLY_TABLES
+        const double2 t = tt[h];
+#else
         const double2 t = T2[h];  // table entries 2h, 2h+1 (shared-memory broadcast)
+#endif
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             const int rho = 2 * h + u;

@@ -1498,6 +1498,8 @@ GatePlan plan_gates(int nl, int n_gates, const int* arity, const int* pos, const
                 else if (lo.kind == kLSignS) code = kCodeSignS;
                 else if (lo.kind == kLSignG) code = kCodeSignG;
                 lo.code = static_cast<std::int8_t>(code | (lo.flush ? kCodeFlush : 0));
+                if (const char* dbg = std::getenv("QRT_DEBUG_PLAN"); dbg && std::atoi(dbg) >= 2)
+                    std::fprintf(stderr, "light op code %d flush %d\n", code, lo.flush ? 1 : 0);
             }
             S.op_count = static_cast<std::int16_t>(n_ops - S.op_begin);
         }

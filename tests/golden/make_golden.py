@@ -14,6 +14,8 @@ product must reproduce:
   and eager), C4 HEA schedules, C5 uniform-word plans (Rng(2024)).
 
     python tests/golden/make_golden.py        # needs oracle/_ref (make -C oracle ref)
+    python tests/golden/make_golden.py configs   # only configs.json
+    python tests/golden/make_golden.py large     # + the 24-qubit reference iterations
 """
 from __future__ import annotations
 
@@ -219,11 +221,32 @@ def configs():
     return out
 
 
+def large():
+    """A 24-qubit full iteration through the reference (GateFabric layers 96 seed 1, JW span-10,
+    p = 8, lazy and eager; ~10 CPU-minutes with 8 workers): GPU parity above the C1 size."""
+    out = {}
+    circ = R.Circuit.gatefabric(24, 96, 1, True)
+    terms = R.Terms.jw(24, 1, 10)
+    for sched in ("flat", "adhoc"):
+        e, a, b = R.evaluate_energy(circ, terms, sched, 8, 0, 0, True, 8)
+        out[f"c24_{sched}_p8"] = {"energy": e, "energy_hex": float(e).hex(), "qsu_qr": a, "evc_qr": b}
+    return out
+
+
 def main():
     if not R.available():
         sys.exit("oracle/_ref/libqrtile_ref.so missing: run `make -C oracle ref` first")
+    if sys.argv[1:] == ["large"]:  # merged into configs.json
+        cfg = json.loads((HERE / "configs.json").read_text())
+        cfg.update(large())
+        (HERE / "configs.json").write_text(json.dumps(cfg, indent=0))
+        return
     if sys.argv[1:] == ["configs"]:
-        (HERE / "configs.json").write_text(json.dumps(configs(), indent=0))
+        cfg = configs()
+        old = HERE / "configs.json"
+        if old.exists():  # keep the (slow) 24-qubit entries of `make_golden.py large`
+            cfg.update({k: v for k, v in json.loads(old.read_text()).items() if k.startswith("c24_")})
+        (HERE / "configs.json").write_text(json.dumps(cfg, indent=0))
         return
     if not R.available():
         sys.exit("oracle/_ref/libqrtile_ref.so missing: run `make -C oracle ref` first")
@@ -231,7 +254,11 @@ def main():
     (HERE / "plans.json").write_text(json.dumps(plans(), indent=0))
     (HERE / "generators.json").write_text(json.dumps(generators(), indent=0))
     (HERE / "distsim.json").write_text(json.dumps(distsim(), indent=0))
-    (HERE / "configs.json").write_text(json.dumps(configs(), indent=0))
+    cfg = configs()
+    old = HERE / "configs.json"
+    if old.exists():  # keep the (slow) 24-qubit entries of `make_golden.py large`
+        cfg.update({k: v for k, v in json.loads(old.read_text()).items() if k.startswith("c24_")})
+    (HERE / "configs.json").write_text(json.dumps(cfg, indent=0))
     print("golden fixtures written to", HERE)
 
 

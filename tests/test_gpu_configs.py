@@ -114,3 +114,24 @@ def test_uniform_words_cross_p(qb, device):
                 assert len(st.qr_log) in (plan.qr_count(), plan.qr_count() + 1)
     for e in energies[1:]:
         assert abs(e - energies[0]) <= 1e-12 * (1 + abs(energies[0])), energies
+
+
+@pytest.mark.parametrize("sched", ["flat", "adhoc"])
+def test_24q_p8_energy_vs_reference(qb, device, sched):
+    """A full 24-qubit iteration (GateFabric layers 96, JW span-10, 8 PEs) against
+    the reference's own evaluate_energy (tests/golden/configs.json, `make_golden.py
+    large`): energy within 1e-10 * (1 + |E|) and the reference's QR counts."""
+    key = f"c24_{sched}_p8"
+    if key not in CFG:
+        pytest.skip("24-qubit reference golden not generated")
+    gold = CFG[key]
+    n = 24
+    c = qb.gen_gatefabric(n, 4 * n, 1, True)
+    d = qb.build_dependency_graph(c)
+    terms = qb.gen_synthetic_jw(n, 1, 10)
+    shape = qb.ClusterShape.flat(8)
+    s = (qb.flat_tiling if sched == "flat" else qb.adhoc_schedule)(c, d, shape)
+    plan = qb.plan_evc(terms, n, shape, True, 8)
+    st, e, qsu, evc = run_iteration(qb, c, s, terms, plan, n, shape)
+    assert abs(e.real - gold["energy"]) <= E_TOL * (1 + abs(gold["energy"])), (e, gold["energy"])
+    assert (qsu, evc) == (gold["qsu_qr"], gold["evc_qr"])

@@ -222,14 +222,20 @@ def configs():
 
 
 def large():
-    """A 24-qubit full iteration through the reference (GateFabric layers 96 seed 1, JW span-10,
-    p = 8, lazy and eager; ~10 CPU-minutes with 8 workers): GPU parity above the C1 size."""
+    """Full iterations through the reference above the C1 size: 24 qubits (GateFabric layers 96
+    seed 1, JW span-10, p = 8, lazy and eager; ~21 CPU-minutes with 8 workers) and 26 qubits
+    (layers 104, lazy; ~45 CPU-minutes)."""
     out = {}
     circ = R.Circuit.gatefabric(24, 96, 1, True)
     terms = R.Terms.jw(24, 1, 10)
     for sched in ("flat", "adhoc"):
         e, a, b = R.evaluate_energy(circ, terms, sched, 8, 0, 0, True, 8)
         out[f"c24_{sched}_p8"] = {"energy": e, "energy_hex": float(e).hex(), "qsu_qr": a, "evc_qr": b}
+    # 26 qubits, lazy only (~45 CPU-minutes with 8 workers)
+    circ = R.Circuit.gatefabric(26, 104, 1, True)
+    terms = R.Terms.jw(26, 1, 10)
+    e, a, b = R.evaluate_energy(circ, terms, "flat", 8, 0, 0, True, 8)
+    out["c26_flat_p8"] = {"energy": e, "energy_hex": float(e).hex(), "qsu_qr": a, "evc_qr": b}
     return out
 
 
@@ -245,7 +251,7 @@ def main():
         cfg = configs()
         old = HERE / "configs.json"
         if old.exists():  # keep the (slow) 24-qubit entries of `make_golden.py large`
-            cfg.update({k: v for k, v in json.loads(old.read_text()).items() if k.startswith("c24_")})
+            cfg.update({k: v for k, v in json.loads(old.read_text()).items() if k.startswith(("c24_", "c26_"))})
         (HERE / "configs.json").write_text(json.dumps(cfg, indent=0))
         return
     if not R.available():
@@ -257,7 +263,7 @@ def main():
     cfg = configs()
     old = HERE / "configs.json"
     if old.exists():  # keep the (slow) 24-qubit entries of `make_golden.py large`
-        cfg.update({k: v for k, v in json.loads(old.read_text()).items() if k.startswith("c24_")})
+        cfg.update({k: v for k, v in json.loads(old.read_text()).items() if k.startswith(("c24_", "c26_"))})
     (HERE / "configs.json").write_text(json.dumps(cfg, indent=0))
     print("golden fixtures written to", HERE)
 

@@ -116,16 +116,16 @@ def test_uniform_words_cross_p(qb, device):
         assert abs(e - energies[0]) <= 1e-12 * (1 + abs(energies[0])), energies
 
 
-@pytest.mark.parametrize("sched", ["flat", "adhoc"])
-def test_24q_p8_energy_vs_reference(qb, device, sched):
-    """A full 24-qubit iteration (GateFabric layers 96, JW span-10, 8 PEs) against
-    the reference's own evaluate_energy (tests/golden/configs.json, `make_golden.py
-    large`): energy within 1e-10 * (1 + |E|) and the reference's QR counts."""
-    key = f"c24_{sched}_p8"
+@pytest.mark.parametrize("n,sched", [(24, "flat"), (24, "adhoc"), (26, "flat")])
+def test_large_p8_energy_vs_reference(qb, device, n, sched):
+    """Full 24- / 26-qubit iterations (GateFabric layers 4n, JW span-10, 8 PEs)
+    against the reference's own evaluate_energy (tests/golden/configs.json,
+    `make_golden.py large`): energy within 1e-10 * (1 + |E|) and the reference's
+    QR counts."""
+    key = f"c{n}_{sched}_p8"
     if key not in CFG:
-        pytest.skip("24-qubit reference golden not generated")
+        pytest.skip(f"{n}-qubit reference golden not generated")
     gold = CFG[key]
-    n = 24
     c = qb.gen_gatefabric(n, 4 * n, 1, True)
     d = qb.build_dependency_graph(c)
     terms = qb.gen_synthetic_jw(n, 1, 10)

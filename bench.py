@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--pes-per-gpu", type=int, default=1,
                     help="PEs per GPU (p = N x this): runs a p-PE schedule (e.g. the p = 8 configs) on fewer GPUs")
     ap.add_argument("--cpu-sample-qubits", type=int, default=24)
+    ap.add_argument("--cpu-full-qubits", type=int, default=20,
+                    help="up to this size the reference arm runs the whole evaluate_energy (measured, C1)")
     return ap.parse_args()
 
 
@@ -204,6 +206,20 @@ def cpu_baseline(args, p, counts=None):
     nproc = os.cpu_count() or 1
     counts = counts or reference_counts(args, p)
     n = counts["n"]
+    if n <= args.cpu_full_qubits:
+        # small enough to run the reference's whole evaluate_energy (dist_sim.cpp:357-363):
+        # measured, not extrapolated (C1: 20 qubits, 4 PEs, full JW ~ 40 s with 4 workers)
+        layers = counts["layers"]
+        circ = R.Circuit.hea(n, layers, 1) if args.circuit == "hea" else R.Circuit.gatefabric(n, layers, 1, True)
+        terms = R.Terms.jw(n, 1, args.span) if args.hamiltonian == "jw" else R.Terms.uniform(n, args.terms, 2024)
+        t0 = time.time()
+        _e, a_qr, b_qr = R.evaluate_energy(circ, terms, args.schedule, p, 0, 0, True, nproc)
+        wall = time.time() - t0
+        return {"value": wall, "unit": "s", "cores": min(nproc, p), "nproc": nproc, "workers": nproc,
+                "kind": "reference", "counts": counts,
+                "sample": f"the reference's full evaluate_energy (oracle/_ref) at n={n}, p={p}, workers={nproc} "
+                          f"(it uses min(workers, p) = {min(nproc, p)} threads; QR 1 thread): measured, "
+                          f"{a_qr} + {b_qr} QRs"}
     ns = min(args.cpu_sample_qubits, n)
     if args.circuit == "hea":
         circ = R.Circuit.hea(ns, 1, 1)

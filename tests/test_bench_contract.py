@@ -21,7 +21,7 @@ def _line(args, timeout=300):
 
 
 def test_reference_arm_contract(ref):
-    d = _line(["--impl", "reference", "--qubits", "16", "--cpu-sample-qubits", "12", "--steps", "1", "--warmup", "0"])
+    d = _line(["--impl", "reference", "--qubits", "16", "--cpu-sample-qubits", "12", "--cpu-full-qubits", "12", "--steps", "1", "--warmup", "0"])
     assert d["impl"] == "reference" and d["unit"] == "s" and d["higher_is_better"] is False
     assert d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     cb = d["cpu_baseline"]
@@ -30,6 +30,17 @@ def test_reference_arm_contract(ref):
     # the reference arm never maps the product's libraries
     assert all("_ref" in so or "oracle" in so for so in d["native_so_loaded"]), d["native_so_loaded"]
     assert d["config"]["qubits"] == 16 and "workload" in d["config"]
+    assert "extrapolated" in cb["sample"]  # 16 > --cpu-full-qubits 12: bounded sample
+
+
+def test_reference_arm_full_run(ref):
+    """Small workloads (n <= --cpu-full-qubits) run the reference's whole
+    evaluate_energy: measured, not extrapolated."""
+    d = _line(["--impl", "reference", "--qubits", "12", "--cpu-full-qubits", "12", "--pes-per-gpu", "4",
+               "--steps", "1", "--warmup", "0"])
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "reference" and "measured" in cb["sample"] and d["value"] > 0
+    assert d["config"]["pes"] == 4
 
 
 @pytest.mark.gpu

@@ -209,6 +209,21 @@ __device__ __forceinline__ void coset_fast(const double2 (&a)[32], const CosetPa
     }
 }
 
+// One group per present mask (CosetSet::tab1 >= 0): the group's rank among
+// the set's fast groups is popc(present below XQ), so its table address needs
+// no per-group metadata load (only the sign masks are read, off the chain).
+template <int XQ>
+__device__ __forceinline__ void coset_fast1(const double2 (&a)[32], const CosetParams& P, const CosetSet& S,
+                                            const double2* __restrict__ tabs, unsigned present, int tab1,
+                                            std::uint64_t W, std::uint64_t pe, double2& acc) {
+    if (!((present >> XQ) & 1u)) return;
+    const int i = __popc(present & ((1u << XQ) - 1u));
+    const double r = coset_group<XQ>(a, tabs + (tab1 >> 1) + 8 * i);
+    const CosetGroup& G = P.groups[S.g_begin + i];
+    const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
+    acc.x += odd ? -r : r;
+}
+
 __device__ __forceinline__ double2 block_sum(double2 v, double2* scratch) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -263,7 +278,24 @@ __device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const doub
         }
         const u64 W = static_cast<u64>(ebase) | wout;
         const unsigned present = S.present;
-        if (present || !P.present_guard) {  // linear-pass sets have no weight-2/4 groups: skip the 15 mask tests
+        const int tab1 = S.tab1;
+        if (P.single && tab1 >= 0) {
+            coset_fast1<3>(a, P, S, stab, present, tab1, W, pe, acc);
+            coset_fast1<5>(a, P, S, stab, present, tab1, W, pe, acc);
+            coset_fast1<6>(a, P, S, stab, present, tab1, W, pe, acc);
+            coset_fast1<9>(a, P, S, stab, present, tab1, W, pe, acc);
+            coset_fast1<10>(a, P, S, stab, present, tab1, W, pe, acc);
+            coset_fast1<12>(a, P, S, stab, present, tab1, W, pe, acc);
+            coset_fast1<15>(a, P, S, stab, present, tab1, W, pe, acc);
+            coset_fast1<17>(a, P, S, stab, present, tab1, W, pe, acc);
+            coset_fast1<18>(a, P, S, stab, present, tab1, W, pe, acc);
+            coset_fast1<20>(a, P, S, stab, present, tab1, W, pe, acc);
+            coset_fast1<23>(a, P, S, stab, present, tab1, W, pe, acc);
+            coset_fast1<24>(a, P, S, stab, present, tab1, W, pe, acc);
+            coset_fast1<27>(a, P, S, stab, present, tab1, W, pe, acc);
+            coset_fast1<29>(a, P, S, stab, present, tab1, W, pe, acc);
+            coset_fast1<30>(a, P, S, stab, present, tab1, W, pe, acc);
+        } else if (present || !P.present_guard) {  // linear-pass sets have no weight-2/4 groups: skip the 15 mask tests
         coset_fast<3>(a, P, S, stab, present, W, pe, acc);
         coset_fast<5>(a, P, S, stab, present, W, pe, acc);
         coset_fast<6>(a, P, S, stab, present, W, pe, acc);
@@ -709,6 +741,11 @@ void launch_coset_pass(CosetParams& P, const CosetDiagTerm* dterms, int pe_count
         return e ? std::atoi(e) : 1;
     }();
     P.present_guard = present_guard;
+    static const int single = [] {
+        const char* e = std::getenv("QRT_EVC_SINGLE");
+        return e ? std::atoi(e) : 1;
+    }();
+    P.single = single;
     // Launches holding only Jordan-Wigner-type groups take the fast-only
     // kernel (218 registers, 2 CTAs/SM; QRT_COSET_OCC=3 squeezes it to 3 CTAs/SM
     // with spills, measured slower); any generic group needs the

@@ -52,6 +52,10 @@ struct CosetSet {
     std::uint16_t eb_lo[16];
     std::uint16_t eb_hi[8];
     std::int16_t swq[kCosetBits];
+    // >= 0: every present fast mask has exactly one group, whose table sits at
+    // tab1 + 16 * popc(present & (2^x - 1)) (no per-group metadata on the table
+    // path, QRT_EVC_SINGLE); -1 otherwise
+    std::int16_t tab1;
 };
 
 // Shared-memory swizzle of tile element e (GF(2)-linear): the host twin of the
@@ -86,6 +90,7 @@ struct CosetParams {
     int n_tab;             // doubles of tabs in use (staged in shared memory)
     int set_tables;        // 1: per-set thread-index / swizzle tables from the host (QRT_EVC_SET_TABLES)
     int present_guard;     // 1: skip a set's weight-2/4 mask tests when it has none (QRT_EVC_PRESENT_GUARD)
+    int single;            // 1: take the tab1 path of sets with one group per fast mask (QRT_EVC_SINGLE)
     int fill_mode;         // 1: pipelined tile fill with warp-reduced base + unrolled linear-swizzle addressing (QRT_EVC_FILL)
     const double* gtabs;   // device copy of tabs[0, n_tab) (coalesced staging)
     // Tile / outer axes as index vectors: element (outer b, tile e) sits at

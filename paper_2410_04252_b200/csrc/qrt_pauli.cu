@@ -756,6 +756,13 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
                     }
                 }
             }
+            {  // one group per present fast mask: tables contiguous in mask order (fast groups first)
+                int nfast = 0;
+                for (std::size_t q = at; q < end; ++q) nfast += fast_of(subs[q]);
+                Sc.tab1 = (nfast > 0 && nfast == __builtin_popcount(Sc.present))
+                              ? P->groups[Sc.g_begin].tab
+                              : static_cast<std::int16_t>(-1);
+            }
             P->sets[P->n_sets++] = Sc;
             P->n_tab = n_tab;
             ++plan.coset_sets;

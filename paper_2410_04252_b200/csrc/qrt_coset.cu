@@ -39,11 +39,29 @@ __host__ __device__ constexpr int ins0(int v, int bit) { return ((v >> bit) << (
 #define QRT_EVC_EARLY_TABLES 1
 #endif
 
+#ifndef QRT_EVC_FMA_SIGN
+#define QRT_EVC_FMA_SIGN 1
+#endif
+#ifndef QRT_EVC_EB_PREFETCH
+#define QRT_EVC_EB_PREFETCH 1
+#endif
+#ifndef QRT_EVC_UNIFORM_PRESENT
+#define QRT_EVC_UNIFORM_PRESENT 1
+#endif
+
 __device__ __forceinline__ double2 lds_f64x2(const double2* p) {
     double2 v;
     const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(a));
     return v;
+}
+
+// (-1)^{popc(W & mf) + popc(pe & gz)} as a double: one POPC of the folded
+// mask, the parity lands in the sign bit (fma(sign, r, acc) == acc +- r exactly).
+__device__ __forceinline__ double group_sign(std::uint64_t W, std::uint64_t pe, const CosetGroup& G) {
+    const std::uint64_t m = (W & G.mf) ^ (pe & G.gz);
+    const unsigned x = static_cast<unsigned>(m) ^ static_cast<unsigned>(m >> 32);
+    return __hiloint2double(static_cast<int>(0x3ff00000u | (static_cast<unsigned>(__popc(x)) << 31)), 0);
 }
 
 template <int XQ>
@@ -163,6 +181,41 @@ __device__ __forceinline__ void coset_ones(const double2 (&a)[32], const CosetPa
     }
 }
 
+// The single single-bit group of mask 1 << K (CosetSet::onemask form): table
+// offset and mode come with the set, so the table loads wait on nothing.
+template <int K>
+__device__ __forceinline__ void coset_one1(const double2 (&a)[32], const CosetParams& P, const CosetSet& S,
+                                           const double* __restrict__ tabs, unsigned onemask, unsigned onemode,
+                                           std::uint64_t W, std::uint64_t pe, double2& acc) {
+    if (!((onemask >> K) & 1u)) return;
+    const int mode = (onemode >> (2 * K)) & 3;
+    const double* T = tabs + S.onetab[K];
+    const CosetGroup& G = P.groups[S.g_begin + __popc(onemask & ((1u << K) - 1u))];
+#if QRT_EVC_FMA_SIGN
+    const double sg = group_sign(W, pe, G);
+    if (mode != 1) {
+        const double2* T2 = reinterpret_cast<const double2*>(T);
+        const double r = mode == 0 ? coset_group<1 << K>(a, T2) : coset_group_im<1 << K>(a, T2);
+        acc.x = fma(sg, r, acc.x);
+    } else {
+        const double2 r = coset_one<1 << K>(a, T, 1);
+        acc.x = fma(sg, r.x, acc.x);
+        acc.y = fma(sg, r.y, acc.y);
+    }
+#else
+    const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
+    if (mode != 1) {
+        const double2* T2 = reinterpret_cast<const double2*>(T);
+        const double r = mode == 0 ? coset_group<1 << K>(a, T2) : coset_group_im<1 << K>(a, T2);
+        acc.x += odd ? -r : r;
+    } else {
+        const double2 r = coset_one<1 << K>(a, T, 1);
+        acc.x += odd ? -r.x : r.x;
+        acc.y += odd ? -r.y : r.y;
+    }
+#endif
+}
+
 // Any flip mask / table mode, pairs read from the shared-memory tile
 // (groups outside the Jordan-Wigner fast set: odd weights, Im(w) terms,
 // complex coefficients).
@@ -220,8 +273,12 @@ __device__ __forceinline__ void coset_fast1(const double2 (&a)[32], const CosetP
     const int i = __popc(present & ((1u << XQ) - 1u));
     const double r = coset_group<XQ>(a, tabs + (tab1 >> 1) + 8 * i);
     const CosetGroup& G = P.groups[S.g_begin + i];
+#if QRT_EVC_FMA_SIGN
+    acc.x = fma(group_sign(W, pe, G), r, acc.x);
+#else
     const int odd = (__popcll(W & G.mf) + __popcll(pe & G.gz)) & 1;
     acc.x += odd ? -r : r;
+#endif
 }
 
 __device__ __forceinline__ double2 block_sum(double2 v, double2* scratch) {
@@ -250,11 +307,24 @@ template <bool GENERIC, bool ONES>
 __device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const double2* __restrict__ tile,
                                                 const double2* __restrict__ stab, int t, u64 wout, u64 pe,
                                                 double2& acc) {
+#if QRT_EVC_EB_PREFETCH
+    // the thread-index tables are per-thread-indexed constant loads (serialised
+    // over distinct addresses): fetch the next set's while this one computes
+    int eb_lo = 0, eb_hi = 0;
+    if (P.set_tables && P.n_sets > 0) {
+        eb_lo = P.sets[0].eb_lo[t & 15];
+        eb_hi = P.sets[0].eb_hi[t >> 4];
+    }
+#endif
     for (int s = 0; s < P.n_sets; ++s) {
         const CosetSet& S = P.sets[s];
         int ebase, swq[kCosetBits];
         if (P.set_tables) {  // host tables (coset_set_tables)
+#if QRT_EVC_EB_PREFETCH
+            ebase = eb_lo | eb_hi;
+#else
             ebase = S.eb_lo[t & 15] | S.eb_hi[t >> 4];
+#endif
 #pragma unroll
             for (int q = 0; q < kCosetBits; ++q) swq[q] = S.swq[q];
         } else {
@@ -277,9 +347,21 @@ __device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const doub
             }
         }
         const u64 W = static_cast<u64>(ebase) | wout;
+#if QRT_EVC_EB_PREFETCH
+        if (P.set_tables && s + 1 < P.n_sets) {
+            eb_lo = P.sets[s + 1].eb_lo[t & 15];
+            eb_hi = P.sets[s + 1].eb_hi[t >> 4];
+        }
+#endif
         const unsigned present = S.present;
         const int tab1 = S.tab1;
         if (P.single && tab1 >= 0) {
+#if QRT_EVC_UNIFORM_PRESENT
+            // warp-uniform by construction; REDUX puts it in a uniform register so the
+            // 15 mask blocks branch without convergence barriers (JW passes 803 -> 782 ms
+            // at 30q; on every set it cost GF(2)-linear passes 1.5%)
+            const unsigned present = __reduce_or_sync(0xffffffffu, S.present);
+#endif
             coset_fast1<3>(a, P, S, stab, present, tab1, W, pe, acc);
             coset_fast1<5>(a, P, S, stab, present, tab1, W, pe, acc);
             coset_fast1<6>(a, P, S, stab, present, tab1, W, pe, acc);
@@ -313,6 +395,17 @@ __device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const doub
         coset_fast<30>(a, P, S, stab, present, W, pe, acc);
         }
         int g1 = S.g_begin + S.xbeg[31];
+        const unsigned onemask = S.onemask;
+        if (ONES && P.single && onemask) {
+            const double* __restrict__ dt = reinterpret_cast<const double*>(stab);
+            const unsigned onemode = S.onemode;
+            coset_one1<0>(a, P, S, dt, onemask, onemode, W, pe, acc);
+            coset_one1<1>(a, P, S, dt, onemask, onemode, W, pe, acc);
+            coset_one1<2>(a, P, S, dt, onemask, onemode, W, pe, acc);
+            coset_one1<3>(a, P, S, dt, onemask, onemode, W, pe, acc);
+            coset_one1<4>(a, P, S, dt, onemask, onemode, W, pe, acc);
+            continue;  // the set holds nothing else
+        }
         if (ONES) {
             const double* __restrict__ dt = reinterpret_cast<const double*>(stab);
             coset_ones<0>(a, P, S, dt, g1, W, pe, acc);

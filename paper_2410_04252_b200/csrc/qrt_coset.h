@@ -56,6 +56,13 @@ struct CosetSet {
     // tab1 + 16 * popc(present & (2^x - 1)) (no per-group metadata on the table
     // path, QRT_EVC_SINGLE); -1 otherwise
     std::int16_t tab1;
+    // >= 0 for every register bit k: the set has no fast groups and exactly one
+    // single-bit group of mask 1 << k for each k with onetab[k] >= 0, whose
+    // table starts at onetab[k] (mode in onemode bits 2k..2k+1); the group's
+    // index is g_begin + popc(onemask below k).  onemask == 0: not this form.
+    std::int16_t onetab[kCosetBits];
+    std::uint8_t onemask;
+    std::uint16_t onemode;
 };
 
 // Shared-memory swizzle of tile element e (GF(2)-linear): the host twin of the

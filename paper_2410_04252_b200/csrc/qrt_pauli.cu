@@ -763,6 +763,26 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
                               ? P->groups[Sc.g_begin].tab
                               : static_cast<std::int16_t>(-1);
             }
+            {  // linear-pass sets: at most one single-bit group per register bit and nothing else
+                Sc.onemask = 0;
+                Sc.onemode = 0;
+                for (int k = 0; k < kCosetBits; ++k) Sc.onetab[k] = -1;
+                bool ok = Sc.present == 0;
+                for (int k = 0; k < kCosetBits; ++k) ok = ok && Sc.one_cnt[k] <= 1;
+                int ng = 0;
+                for (int k = 0; k < kCosetBits; ++k) ng += Sc.one_cnt[k];
+                ok = ok && ng == Sc.g_count && ng > 0;
+                if (ok) {
+                    int g = Sc.g_begin;
+                    for (int k = 0; k < kCosetBits; ++k)
+                        if (Sc.one_cnt[k]) {
+                            const CosetGroup& G = P->groups[g++];
+                            Sc.onemask |= static_cast<std::uint8_t>(1u << k);
+                            Sc.onetab[k] = G.tab;
+                            Sc.onemode |= static_cast<std::uint16_t>((G.mode & 3) << (2 * k));
+                        }
+                }
+            }
             P->sets[P->n_sets++] = Sc;
             P->n_tab = n_tab;
             ++plan.coset_sets;

@@ -7,6 +7,10 @@
 #include "qrt_fused.h"
 #include "qrt_light.h"
 
+#ifndef QRT_LIGHT_PREFETCH
+#define QRT_LIGHT_PREFETCH 1
+#endif
+
 namespace qrt {
 
 namespace {
@@ -267,26 +271,39 @@ __global__ void __launch_bounds__(kLightThreads, 2)
         }
         const u64 W = static_cast<u64>(ebase) | wout;
         const int o_end = S.op_begin + S.op_count;
+#if QRT_LIGHT_PREFETCH
+        // the next op's dispatch code is loaded while this op computes (it heads
+        // each op's load chain: code -> dispatch -> matrix offset -> matrix)
+        int code_n = 0;
+        if (S.op_count > 0) code_n = P.ops[S.op_begin].code;
+#endif
         for (int o = S.op_begin; o < o_end; ++o) {
             const LightOp& op = P.ops[o];
             // one host-computed case code per op (jump table), flush bit on top
+#if QRT_LIGHT_PREFETCH
+            const int code = code_n;
+            const int mat = op.mat;
+            if (o + 1 < o_end) code_n = P.ops[o + 1].code;
+#else
             const int code = op.code;
+            const int mat = op.mat;
+#endif
             if (code & kCodeFlush) apply_signs(a, pend);
             switch (code & ~kCodeFlush) {
-                case 0: dense1<0>(a, P.mats + op.mat); break;
-                case 1: dense1<1>(a, P.mats + op.mat); break;
-                case 2: dense1<2>(a, P.mats + op.mat); break;
-                case 3: dense1<3>(a, P.mats + op.mat); break;
-                case 4: dense2<0, 1>(a, P.mats + op.mat); break;
-                case 5: dense2<0, 2>(a, P.mats + op.mat); break;
-                case 6: dense2<0, 3>(a, P.mats + op.mat); break;
-                case 7: dense2<1, 2>(a, P.mats + op.mat); break;
-                case 8: dense2<1, 3>(a, P.mats + op.mat); break;
-                case 9: dense2<2, 3>(a, P.mats + op.mat); break;
-                case kCodeReal1 + 0: dense1r<0>(a, P.mats + op.mat); break;
-                case kCodeReal1 + 1: dense1r<1>(a, P.mats + op.mat); break;
-                case kCodeReal1 + 2: dense1r<2>(a, P.mats + op.mat); break;
-                case kCodeReal1 + 3: dense1r<3>(a, P.mats + op.mat); break;
+                case 0: dense1<0>(a, P.mats + mat); break;
+                case 1: dense1<1>(a, P.mats + mat); break;
+                case 2: dense1<2>(a, P.mats + mat); break;
+                case 3: dense1<3>(a, P.mats + mat); break;
+                case 4: dense2<0, 1>(a, P.mats + mat); break;
+                case 5: dense2<0, 2>(a, P.mats + mat); break;
+                case 6: dense2<0, 3>(a, P.mats + mat); break;
+                case 7: dense2<1, 2>(a, P.mats + mat); break;
+                case 8: dense2<1, 3>(a, P.mats + mat); break;
+                case 9: dense2<2, 3>(a, P.mats + mat); break;
+                case kCodeReal1 + 0: dense1r<0>(a, P.mats + mat); break;
+                case kCodeReal1 + 1: dense1r<1>(a, P.mats + mat); break;
+                case kCodeReal1 + 2: dense1r<2>(a, P.mats + mat); break;
+                case kCodeReal1 + 3: dense1r<3>(a, P.mats + mat); break;
                 case kCodeSignU: g ^= static_cast<unsigned>(op.tab >> fixed_value(op, W)) & 1u; break;
                 case kCodeSignS: pend ^= static_cast<unsigned>(op.tab >> (16 * fixed_value(op, W))) & 0xffffu; break;
                 case kCodeSignG: {
@@ -301,7 +318,7 @@ __global__ void __launch_bounds__(kLightThreads, 2)
                 default: {
                     // phase diagonal (k <= 2): two entries live at a time
                     const int f = fixed_value(op, W);
-                    const double2* d = P.mats + op.mat;
+                    const double2* d = P.mats + mat;
                     const int halves = op.k > 1 ? 2 : 1;
 #pragma unroll 1
                     for (int hb = 0; hb < halves; ++hb) {

@@ -1372,6 +1372,13 @@ void pauli_plan_info(int nl, int n_terms, const std::uint64_t* x, const std::uin
                 ++dpasses;
                 dwords += cp->d_count;
             }
+        int tab1_sets = 0, one_sets = 0;
+        for (const auto& cp : plan.cosets)
+            for (int si = 0; si < cp->n_sets; ++si) {
+                tab1_sets += cp->sets[si].tab1 >= 0;
+                one_sets += cp->sets[si].onemask != 0;
+            }
+        std::fprintf(stderr, "evc cosets: table-path sets %d fast / %d single-bit\n", tab1_sets, one_sets);
         std::fprintf(stderr, "evc cosets: %d I/Z words in %d passes; %d sets, %d fast groups over %d (set, mask) pairs; "
                      "per-pair counts 1..7+:", dwords, dpasses, sets, fast, distinct);
         for (int i = 1; i < 8; ++i) std::fprintf(stderr, " %d", hist[i]);

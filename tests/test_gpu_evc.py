@@ -90,7 +90,7 @@ def test_coset_deterministic(qb, device):
                                  {"QRT_QR_PUSH": "1", "QRT_FUSED_QR": "0", "QRT_QR_INPLACE": "0"},
                                  {"QRT_FUSED_QR": "0"}, {"QRT_EVC_SET_TABLES": "0"}, {"QRT_EVC_PRESENT_GUARD": "0"},
                                  {"QRT_EVC_FILL": "1"}, {"QRT_EVC_TEAMS": "1"}, {"QRT_EVC_PLAN_BATCHED": "0"},
-                                 {"QRT_EVC_LINEAR_COAL": "3"}])
+                                 {"QRT_EVC_LINEAR_COAL": "3"}, {"QRT_EVC_SINGLE": "0"}])
 def test_knobs_in_subprocess(env):
     """Knobs read once per process: a fresh process per setting, checked
     against the oracle (GateFabric QSU + JW EVC at 16 qubits, 2 PEs)."""

@@ -64,9 +64,36 @@ __device__ __forceinline__ double group_sign(std::uint64_t W, std::uint64_t pe, 
     return __hiloint2double(static_cast<int>(0x3ff00000u | (static_cast<unsigned>(__popc(x)) << 31)), 0);
 }
 
+#ifndef QRT_EVC_ACCS
+#define QRT_EVC_ACCS 4  // independent accumulator chains per group (2 / 8: see DESIGN §8)
+#endif
+
 template <int XQ>
 __device__ __forceinline__ double coset_group(const double2 (&a)[32], const double2* __restrict__ T2) {
     constexpr int H = top_bit(XQ);
+#if QRT_EVC_ACCS != 4
+    constexpr int NA = QRT_EVC_ACCS;
+    double accn[NA];
+#pragma unroll
+    for (int i = 0; i < NA; ++i) accn[i] = 0.0;
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+        const double2 t = lds_f64x2(T2 + h);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int rho = 2 * h + u;
+            const int r = ins0(rho, H);
+            const int s = r ^ XQ;
+            const double2 A = a[s], B = a[r];
+            accn[rho % NA] = fma(u ? t.y : t.x, fma(A.x, B.x, A.y * B.y), accn[rho % NA]);
+        }
+    }
+#pragma unroll
+    for (int w = NA / 2; w > 0; w >>= 1)
+#pragma unroll
+        for (int i = 0; i < w; ++i) accn[i] += accn[i + w];
+    return accn[0];
+#else
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #if QRT_EVC_EARLY_TABLES
     double2 tt[8];
@@ -90,6 +117,7 @@ __device__ __forceinline__ double coset_group(const double2 (&a)[32], const doub
         }
     }
     return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#endif
 }
 
 // Single-bit register mask XQ (linear passes), any table mode: the 16 pairs

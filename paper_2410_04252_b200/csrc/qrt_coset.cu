@@ -34,9 +34,12 @@ __host__ __device__ constexpr int ins0(int v, int bit) { return ((v >> bit) << (
 // QRT_EVC_EARLY_TABLES: issue the group's 8 table loads (LDS.128) before the
 // pair products, pinned by volatile asm, so their latency overlaps the DMUL /
 // DFMA work instead of stalling the accumulation chains (the compiler places
-// them after the products to save registers).
+// them after the products to save registers).  Kept on while the table
+// address came from a per-group record (JW -0.4%); with the table path
+// (CosetSet::tab1) the compiler's own placement is faster: 30q JW EVC
+// 767 -> 749 ms (same-box A/B, profiles/r2/evcvar), so it is off.
 #ifndef QRT_EVC_EARLY_TABLES
-#define QRT_EVC_EARLY_TABLES 1
+#define QRT_EVC_EARLY_TABLES 0
 #endif
 
 #ifndef QRT_EVC_FMA_SIGN

@@ -42,6 +42,9 @@ __host__ __device__ constexpr int ins0(int v, int bit) { return ((v >> bit) << (
 #define QRT_EVC_EARLY_TABLES 0
 #endif
 
+#ifndef QRT_EVC_THREAD_ACC
+#define QRT_EVC_THREAD_ACC 0
+#endif
 #ifndef QRT_EVC_FMA_SIGN
 #define QRT_EVC_FMA_SIGN 1
 #endif
@@ -293,6 +296,39 @@ __device__ __forceinline__ void coset_fast(const double2 (&a)[32], const CosetPa
     }
 }
 
+#if QRT_EVC_THREAD_ACC
+// Table path with the group sign moved onto the table entries (an integer XOR
+// of their sign bits) and the products accumulated into four per-thread
+// chains that run across groups and sets: no per-group tree or sign tail.
+template <int XQ>
+__device__ __forceinline__ void coset_fast1t(const double2 (&a)[32], const CosetParams& P, const CosetSet& S,
+                                             const double2* __restrict__ tabs, unsigned present, int tab1,
+                                             std::uint64_t W, std::uint64_t pe, double (&acc4)[4]) {
+    if (!((present >> XQ) & 1u)) return;
+    constexpr int H = top_bit(XQ);
+    const int i = __popc(present & ((1u << XQ) - 1u));
+    const CosetGroup& G = P.groups[S.g_begin + i];
+    const std::uint64_t m = (W & G.mf) ^ (pe & G.gz);
+    const int sb = static_cast<int>(static_cast<unsigned>(__popc(static_cast<unsigned>(m) ^
+                                                                 static_cast<unsigned>(m >> 32))) << 31);
+    const double2* __restrict__ T2 = tabs + (tab1 >> 1) + 8 * i;
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+        const double2 t = T2[h];
+        const double tx = __hiloint2double(__double2hiint(t.x) ^ sb, __double2loint(t.x));
+        const double ty = __hiloint2double(__double2hiint(t.y) ^ sb, __double2loint(t.y));
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int rho = 2 * h + u;
+            const int r = ins0(rho, H);
+            const int s = r ^ XQ;
+            const double2 A = a[s], B = a[r];
+            acc4[rho & 3] = fma(u ? ty : tx, fma(A.x, B.x, A.y * B.y), acc4[rho & 3]);
+        }
+    }
+}
+#endif
+
 // One group per present mask (CosetSet::tab1 >= 0): the group's rank among
 // the set's fast groups is popc(present below XQ), so its table address needs
 // no per-group metadata load (only the sign masks are read, off the chain).
@@ -338,6 +374,9 @@ template <bool GENERIC, bool ONES>
 __device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const double2* __restrict__ tile,
                                                 const double2* __restrict__ stab, int t, u64 wout, u64 pe,
                                                 double2& acc) {
+#if QRT_EVC_THREAD_ACC
+    double acc4[4] = {0.0, 0.0, 0.0, 0.0};
+#endif
 #if QRT_EVC_EB_PREFETCH
     // the thread-index tables are per-thread-indexed constant loads (serialised
     // over distinct addresses): fetch the next set's while this one computes
@@ -393,6 +432,23 @@ __device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const doub
             // at 30q; on every set it cost GF(2)-linear passes 1.5%)
             const unsigned present = __reduce_or_sync(0xffffffffu, S.present);
 #endif
+#if QRT_EVC_THREAD_ACC
+            coset_fast1t<3>(a, P, S, stab, present, tab1, W, pe, acc4);
+            coset_fast1t<5>(a, P, S, stab, present, tab1, W, pe, acc4);
+            coset_fast1t<6>(a, P, S, stab, present, tab1, W, pe, acc4);
+            coset_fast1t<9>(a, P, S, stab, present, tab1, W, pe, acc4);
+            coset_fast1t<10>(a, P, S, stab, present, tab1, W, pe, acc4);
+            coset_fast1t<12>(a, P, S, stab, present, tab1, W, pe, acc4);
+            coset_fast1t<15>(a, P, S, stab, present, tab1, W, pe, acc4);
+            coset_fast1t<17>(a, P, S, stab, present, tab1, W, pe, acc4);
+            coset_fast1t<18>(a, P, S, stab, present, tab1, W, pe, acc4);
+            coset_fast1t<20>(a, P, S, stab, present, tab1, W, pe, acc4);
+            coset_fast1t<23>(a, P, S, stab, present, tab1, W, pe, acc4);
+            coset_fast1t<24>(a, P, S, stab, present, tab1, W, pe, acc4);
+            coset_fast1t<27>(a, P, S, stab, present, tab1, W, pe, acc4);
+            coset_fast1t<29>(a, P, S, stab, present, tab1, W, pe, acc4);
+            coset_fast1t<30>(a, P, S, stab, present, tab1, W, pe, acc4);
+#else
             coset_fast1<3>(a, P, S, stab, present, tab1, W, pe, acc);
             coset_fast1<5>(a, P, S, stab, present, tab1, W, pe, acc);
             coset_fast1<6>(a, P, S, stab, present, tab1, W, pe, acc);
@@ -408,6 +464,7 @@ __device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const doub
             coset_fast1<27>(a, P, S, stab, present, tab1, W, pe, acc);
             coset_fast1<29>(a, P, S, stab, present, tab1, W, pe, acc);
             coset_fast1<30>(a, P, S, stab, present, tab1, W, pe, acc);
+#endif
         } else if (present || !P.present_guard) {  // linear-pass sets have no weight-2/4 groups: skip the 15 mask tests
         coset_fast<3>(a, P, S, stab, present, W, pe, acc);
         coset_fast<5>(a, P, S, stab, present, W, pe, acc);
@@ -454,6 +511,9 @@ __device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const doub
             acc.y += odd ? -r.y : r.y;
         }
     }
+#if QRT_EVC_THREAD_ACC
+    acc.x += (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+#endif
 }
 
 template <int MINB, bool GENERIC, bool ONES>

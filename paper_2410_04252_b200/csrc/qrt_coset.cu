@@ -42,6 +42,9 @@ __host__ __device__ constexpr int ins0(int v, int bit) { return ((v >> bit) << (
 #define QRT_EVC_EARLY_TABLES 0
 #endif
 
+#ifndef QRT_EVC_BYTE_GATHER
+#define QRT_EVC_BYTE_GATHER 1
+#endif
 #ifndef QRT_EVC_THREAD_ACC
 #define QRT_EVC_THREAD_ACC 0
 #endif
@@ -406,6 +409,27 @@ __device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const doub
         }
         const int sb = swz(ebase);
         double2 a[32];
+#if QRT_EVC_BYTE_GATHER
+        {
+            // byte offsets from the dynamic shared-memory base, XOR-composed (swz is
+            // GF(2)-linear, x16 distributes over XOR, and the tile's own offset is a
+            // multiple of 64 KiB): one LOP3 per amplitude, the base an immediate
+            extern __shared__ __align__(16) unsigned char smem_raw[];
+            const unsigned toff = static_cast<unsigned>(reinterpret_cast<const unsigned char*>(tile) - smem_raw);
+            unsigned qb[kCosetBits];
+#pragma unroll
+            for (int q = 0; q < kCosetBits; ++q) qb[q] = static_cast<unsigned>(swq[q]) << 4;
+            const unsigned sbb = toff | (static_cast<unsigned>(sb) << 4);
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+                unsigned o = sbb;
+#pragma unroll
+                for (int q = 0; q < kCosetBits; ++q)
+                    if ((r >> q) & 1) o ^= qb[q];
+                a[r] = *reinterpret_cast<const double2*>(smem_raw + o);
+            }
+        }
+#else
         {
 #pragma unroll
             for (int r = 0; r < 32; ++r) {
@@ -416,6 +440,7 @@ __device__ __forceinline__ void coset_tile_sets(const CosetParams& P, const doub
                 a[r] = tile[o];
             }
         }
+#endif
         const u64 W = static_cast<u64>(ebase) | wout;
 #if QRT_EVC_EB_PREFETCH
         if (P.set_tables && s + 1 < P.n_sets) {

@@ -42,6 +42,9 @@ __host__ __device__ constexpr int ins0(int v, int bit) { return ((v >> bit) << (
 #define QRT_EVC_EARLY_TABLES 0
 #endif
 
+#ifndef QRT_EVC_PE_FOLD
+#define QRT_EVC_PE_FOLD 1
+#endif
 #ifndef QRT_EVC_BYTE_GATHER
 #define QRT_EVC_BYTE_GATHER 1
 #endif
@@ -68,7 +71,11 @@ __device__ __forceinline__ double2 lds_f64x2(const double2* p) {
 // (-1)^{popc(W & mf) + popc(pe & gz)} as a double: one POPC of the folded
 // mask, the parity lands in the sign bit (fma(sign, r, acc) == acc +- r exactly).
 __device__ __forceinline__ double group_sign(std::uint64_t W, std::uint64_t pe, const CosetGroup& G) {
+#if QRT_EVC_PE_FOLD
+    const std::uint64_t m = (W | (pe << kCosetPeShift)) & G.mf;  // gz rides in mf above bit 40
+#else
     const std::uint64_t m = (W & G.mf) ^ (pe & G.gz);
+#endif
     const unsigned x = static_cast<unsigned>(m) ^ static_cast<unsigned>(m >> 32);
     return __hiloint2double(static_cast<int>(0x3ff00000u | (static_cast<unsigned>(__popc(x)) << 31)), 0);
 }

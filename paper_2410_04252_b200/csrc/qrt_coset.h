@@ -29,8 +29,12 @@ inline constexpr int kCosetMaxSets = 40;
 inline constexpr int kCosetMaxGroups = 320;
 inline constexpr int kCosetMaxTab = 2048;  // doubles in the launch parameters
 
+// CosetGroup::mf also carries gz shifted to this bit (W < 2^n_local <= 2^40
+// never reaches it), so W | pe << kCosetPeShift folds both sign masks into one.
+inline constexpr int kCosetPeShift = 40;
+
 struct CosetGroup {
-    std::uint64_t mf;  // sign bits outside Q, as bits of the thread word W
+    std::uint64_t mf;  // sign bits outside Q, as bits of the thread word W (| gz << kCosetPeShift)
     std::uint64_t gz;  // sign bits over the PE index
     std::int16_t tab;  // first double of the group's table(s) in CosetParams::tabs
     std::int8_t xq;    // flip mask over the coset's register bits (nonzero)

@@ -725,7 +725,9 @@ void build_coset_pass(PauliPlanHost& plan, int nl, int pe_begin, std::uint64_t B
                 const Sub& u = subs[q];
                 CosetGroup& G = P->groups[n_groups++];
                 G.xq = static_cast<std::int8_t>(u.xq);
-                G.mf = u.mf;
+                if (nl > kCosetPeShift || (u.gz >> (64 - kCosetPeShift)) != 0)
+                    fail(QRT_ERR_INVALID, "EVC sign masks exceed the folded layout");
+                G.mf = u.mf | (u.gz << kCosetPeShift);
                 G.gz = u.gz;
                 G.tab = static_cast<std::int16_t>(n_tab);
                 const bool re_real = re_real_of(u);

@@ -1,5 +1,5 @@
 #!/bin/bash
-# Same-box A/B: coset gathers with XOR-composed byte offsets from the shared base (product) vs libqrt_nofold.so
+# Same-box A/B: PE sign mask folded into the group mf (product) vs libqrt_nofold.so
 O=${OUT:-gpurun_out/fold}; mkdir -p $O
 timeout 1200 python -m pytest tests/test_gpu_evc.py tests/test_gpu_configs.py tests/test_gpu_parity.py tests/test_gpu_abi.py -q -m gpu > $O/tests.log 2>&1; echo rc=$? >> $O/tests.log
 P=$PWD/paper_2410_04252_b200
